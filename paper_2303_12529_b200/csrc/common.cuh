@@ -1,0 +1,89 @@
+// Shared device helpers: complex arithmetic on float2/double2, precision
+// traits, deterministic block reductions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math_constants.h>
+
+#define LS_HD __host__ __device__ __forceinline__
+#define LS_D __device__ __forceinline__
+
+template <typename R> struct CT;
+template <> struct CT<float> { using C = float2; };
+template <> struct CT<double> { using C = double2; };
+
+LS_HD float2 cmk(float a, float b) { return make_float2(a, b); }
+LS_HD double2 cmk(double a, double b) { return make_double2(a, b); }
+LS_HD float2 operator+(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+LS_HD double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+LS_HD float2 operator-(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+LS_HD double2 operator-(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+LS_HD float2 operator*(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+LS_HD double2 operator*(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+template <typename C> LS_HD C cmul(C a, C b) {
+  return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename C> LS_HD C cmulc(C a, C b) {
+  return cmk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename C> LS_HD C cconj(C a) { return cmk(a.x, -a.y); }
+// multiply by -i (forward-sign quarter turn)
+template <typename C> LS_HD C mul_mi(C a) { return cmk(a.y, -a.x); }
+
+// ---------------------------------------------------------------------------
+// deterministic reductions: warp shuffle -> smem -> one value per block; the
+// per-block partials are combined later by a single block in fixed order.
+
+template <typename T> LS_D T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T> LS_D T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block sum of NV values per thread; result valid in thread 0.  `red` must
+// hold NV * 32 entries.  Fixed combination order -> bit-reproducible.
+template <int NV> LS_D void block_sum(double (&v)[NV], double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[i * 32 + warp] = v[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double t = lane < nw ? red[i * 32 + lane] : 0.0;
+      v[i] = warp_sum(t);
+    }
+  }
+}
+template <int NV> LS_D void block_max(double (&v)[NV], double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_max(v[i]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[i * 32 + warp] = v[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double t = lane < nw ? red[i * 32 + lane] : 0.0;
+      v[i] = warp_max(t);
+    }
+  }
+}

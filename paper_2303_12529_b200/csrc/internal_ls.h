@@ -1,0 +1,55 @@
+// Level-set / loop-control launchers and the device-resident loop state.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+namespace lsb {
+
+// Device-resident state of the DSO loop (optimizer.py:230-269).  Every kernel
+// of an iteration reads `stopped` first, so the host can enqueue iterations
+// without waiting for the stop rule.
+struct DevState {
+  double best, l_ilt, l_pvb, l_dso;
+  double beta;
+  double vmax, gmax, dt;
+  int stopped, improved, use_beta, streak, nhist, nonfinite_it;
+};
+
+struct LoopCfg {
+  double alpha, beta, stop_rel_tol;
+  int stop_patience;
+};
+
+enum EwOp { EW_MASK = 1, EW_HEAVISIDE, EW_AXPBY, EW_SIGMOID, EW_HARD, EW_NEG, EW_CG, EW_MOTION, EW_EVOLVE, EW_AHF, EW_HYPOT };
+enum RdOp { RD_SUMSQDIFF = 1, RD_DOT, RD_DOTDIFF, RD_MAXABS, RD_COUNTNEQ8, RD_NONFINITE, RD_COUNTNEQ };
+
+int ls_blocks();
+void launch_geometry(int H, int W, const double* phi, double* gx, double* gy, double* gxx, double* gyy,
+                     double* gxy, double* mag, cudaStream_t s);
+void launch_curvature(int H, int W, const double* phi, const double* m, double weight, double* out,
+                      cudaStream_t s);
+void launch_ls_velocity(int H, int W, const double* phi, const double* v, const double* dprev, const double* m,
+                        double weight, int use_curv, const DevState* st, double* d, double* u, double* gm,
+                        double* partials, cudaStream_t s);
+void launch_ls_update(size_t n, double* phi, const double* u, const double* gm, double lo, double hi,
+                      const DevState* st, uint8_t* mask, double* partials, cudaStream_t s);
+void launch_copy_best(size_t n, const double* phi, double* best, const DevState* st, cudaStream_t s);
+void launch_after_forward(const double* part, int nb, LoopCfg c, int it, DevState* st, double* hist,
+                          cudaStream_t s);
+void launch_after_grad(const double* dots, int nb, int restart, DevState* st, cudaStream_t s);
+void launch_after_velocity(const double* part, int nb, double eta, DevState* st, double* hist, cudaStream_t s);
+void launch_after_update(const double* part, int nb, DevState* st, double* hist, cudaStream_t s);
+void launch_elementwise(int op, size_t n, const double* a, const double* b, double p0, double p1, double p2,
+                        double* out, uint8_t* out8, cudaStream_t s);
+// out: device scalar
+void launch_reduce(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
+                   double* partials, double* out, cudaStream_t s);
+
+// exact EDT -> truncated signed distance (levelset.py:86-101)
+void launch_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_lower, double* phi,
+                 int* scratch_i32, double* scratch_f64, cudaStream_t s);
+size_t tsdf_scratch_i32(int H, int W);
+size_t tsdf_scratch_f64(int H, int W);
+
+}  // namespace lsb

@@ -1,0 +1,697 @@
+// C ABI (include/lsopc_b200.h): plans, device spectra, the operator entry
+// points, and the on-device DSO loop driver (optimizer.py:204-284).
+#include "internal.h"
+#include "internal_ls.h"
+#include "../../include/lsopc_b200.h"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace lsb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(LSOPC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ck_launch(const char* what) { ck(cudaGetLastError(), what); }
+
+template <class F> int guarded(F&& f) {
+  try {
+    f();
+    return LSOPC_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LSOPC_EINVAL;
+  }
+}
+
+bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+int ilog2(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    cap = bytes;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct lsopc_plan {
+  Grid g{};
+  DevBuf tw, tw64, mhat, scratch, G, If, Id, wf, wd, partials, scal, A, hard, tsdf_i, tsdf_f;
+  ~lsopc_plan() {
+    for (DevBuf* b : {&tw, &tw64, &mhat, &scratch, &G, &If, &Id, &wf, &wd, &partials, &scal, &A, &hard, &tsdf_i,
+                      &tsdf_f})
+      b->release();
+  }
+  size_t n() const { return g.n(); }
+};
+
+struct lsopc_kset {
+  lsopc_plan* plan = nullptr;
+  int nk = 0, K = 0;
+  DevBuf spec;
+  std::vector<double> w;
+  ~lsopc_kset() { spec.release(); }
+};
+
+namespace {
+
+void check_plan(const lsopc_plan* p) {
+  if (!p) throw Error(LSOPC_EINVAL, "null plan");
+}
+void check_kset(const lsopc_plan* p, const lsopc_kset* k) {
+  if (!k || k->plan != p) throw Error(LSOPC_EINVAL, "kernel set does not belong to this plan");
+}
+
+double reduce_to_host(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
+                      lsopc_plan* plan, cudaStream_t s) {
+  DevBuf tmp;
+  double* part;
+  double* out;
+  if (plan) {
+    part = plan->partials.as<double>();
+    out = plan->scal.as<double>();
+  } else {
+    tmp.ensure((ls_blocks() + 8) * sizeof(double));
+    part = tmp.as<double>();
+    out = part + ls_blocks();
+  }
+  launch_reduce(op, n, a, b, a8, b8, part, out, s);
+  ck_launch("reduce");
+  double h = 0.0;
+  ck(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, s), "memcpy");
+  ck(cudaStreamSynchronize(s), "sync");
+  tmp.release();
+  return h;
+}
+
+// forward of one set into If/Id with (optional) field storage at A offset
+void forward(lsopc_plan* p, const lsopc_kset* ks, void* I, void* A, StopFlag stop, cudaStream_t s) {
+  launch_forward_set(p->g, ks->nk, p->mhat.p, ks->spec.p, ks->w.data(), A, I, p->scratch.p, stop, s);
+  ck_launch("forward");
+}
+
+}  // namespace
+
+// ============================================================================
+
+extern "C" {
+
+const char* lsopc_last_error(void) { return g_err.c_str(); }
+int lsopc_abi_version(void) { return 1; }
+
+int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
+  return guarded([&] {
+    if (!out) throw Error(LSOPC_EINVAL, "null output");
+    if (!pow2(H) || !pow2(W) || H < 4 || W < 4 || H > 8192 || W > 8192 || (size_t)H * W < 16)
+      throw Error(LSOPC_EINVAL, "grid " + std::to_string(W) + "x" + std::to_string(H) +
+                                    " unsupported: sides must be powers of two in [4, 8192]");
+    if (precision != LSOPC_FP32 && precision != LSOPC_FP64) throw Error(LSOPC_EINVAL, "bad precision");
+    auto* p = new lsopc_plan();
+    try {
+      p->g.H = H;
+      p->g.W = W;
+      p->g.lgH = ilog2(H);
+      p->g.lgW = ilog2(W);
+      p->g.prec = precision;
+      const int nmax = H > W ? H : W;
+      p->g.lgnmax = ilog2(nmax);
+      std::vector<double> t64(2 * nmax);
+      std::vector<float> t32(2 * nmax);
+      for (int j = 0; j < nmax; ++j) {
+        long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)j / (long double)nmax;
+        t64[2 * j] = (double)cosl(a);
+        t64[2 * j + 1] = (double)sinl(a);
+        t32[2 * j] = (float)cosl(a);
+        t32[2 * j + 1] = (float)sinl(a);
+      }
+      p->tw64.ensure(t64.size() * sizeof(double));
+      ck(cudaMemcpy(p->tw64.p, t64.data(), t64.size() * sizeof(double), cudaMemcpyHostToDevice), "memcpy");
+      if (precision == LSOPC_FP64) {
+        p->g.tw = p->tw64.p;
+      } else {
+        p->tw.ensure(t32.size() * sizeof(float));
+        ck(cudaMemcpy(p->tw.p, t32.data(), t32.size() * sizeof(float), cudaMemcpyHostToDevice), "memcpy");
+        p->g.tw = p->tw.p;
+      }
+      p->g.tw64 = p->tw64.p;
+      const size_t n = p->n();
+      p->mhat.ensure(n * p->g.csize());
+      p->scratch.ensure(n * 16);
+      p->G.ensure(n * p->g.csize());
+      p->If.ensure(n * p->g.rsize());
+      p->Id.ensure(n * p->g.rsize());
+      p->wf.ensure(n * p->g.rsize());
+      p->wd.ensure(n * p->g.rsize());
+      size_t np = (size_t)std::max(std::max(reduce_blocks(), ls_blocks()), H) * 2 + 64;
+      p->partials.ensure(np * sizeof(double));
+      p->scal.ensure(64 * sizeof(double));
+      p->hard.ensure(3 * n);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int lsopc_plan_destroy(lsopc_plan* plan) {
+  return guarded([&] {
+    cudaDeviceSynchronize();
+    delete plan;
+  });
+}
+
+int lsopc_kset_create(lsopc_plan* plan, int n_k, int K, const double* coeffs_host, const double* weights_host,
+                      void* stream, lsopc_kset** out) {
+  return guarded([&] {
+    check_plan(plan);
+    if (n_k < 1 || K < 1) throw Error(LSOPC_EINVAL, "kernel set must contain at least one kernel");
+    if (K > plan->g.H || K > plan->g.W)
+      throw Error(LSOPC_EINVAL, "kernel side " + std::to_string(K) + " exceeds grid " + std::to_string(plan->g.W) +
+                                    "x" + std::to_string(plan->g.H));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto* ks = new lsopc_kset();
+    try {
+      ks->plan = plan;
+      ks->nk = n_k;
+      ks->K = K;
+      ks->w.assign(weights_host, weights_host + n_k);
+      ks->spec.ensure((size_t)n_k * plan->n() * plan->g.csize());
+      DevBuf coeffs;
+      const size_t cb = (size_t)n_k * K * K * 2 * sizeof(double);
+      coeffs.ensure(cb);
+      ck(cudaMemcpyAsync(coeffs.p, coeffs_host, cb, cudaMemcpyHostToDevice, s), "memcpy");
+      launch_kernel_spectra(plan->g, n_k, K, coeffs.as<double>(), ks->spec.p, plan->scratch.p, s);
+      ck_launch("kernel spectra");
+      ck(cudaStreamSynchronize(s), "sync");
+      coeffs.release();
+    } catch (...) {
+      delete ks;
+      throw;
+    }
+    *out = ks;
+  });
+}
+
+int lsopc_kset_download(const lsopc_kset* ks, double* out, void* stream) {
+  return guarded([&] {
+    if (!ks) throw Error(LSOPC_EINVAL, "null kernel set");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t n = ks->plan->n();
+    Grid g = ks->plan->g;
+    for (int k = 0; k < ks->nk; ++k) {
+      launch_to_c128(g, static_cast<const char*>(ks->spec.p) + (size_t)k * n * g.csize(), out + (size_t)k * n * 2, s);
+      ck_launch("download");
+    }
+  });
+}
+
+int lsopc_kset_destroy(lsopc_kset* ks) {
+  return guarded([&] {
+    cudaDeviceSynchronize();
+    delete ks;
+  });
+}
+
+int lsopc_aerial_intensity(lsopc_plan* plan, const lsopc_kset* ks, const double* mask_dev, double dose,
+                           double* out_dev, void* stream) {
+  return guarded([&] {
+    check_plan(plan);
+    check_kset(plan, ks);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    launch_mask_fft(plan->g, nullptr, mask_dev, plan->mhat.p, plan->scratch.p, nullptr, s);
+    ck_launch("mask fft");
+    forward(plan, ks, plan->If.p, nullptr, nullptr, s);
+    launch_scale_intensity(plan->g, plan->If.p, dose, out_dev, s);
+    ck_launch("scale intensity");
+  });
+}
+
+int lsopc_print_corners(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_kset* defocus,
+                        const double* mask_dev, double i_th, double sigma_z, int binarize, void* nom, void* inner,
+                        void* outer, void* stream) {
+  return guarded([&] {
+    check_plan(plan);
+    check_kset(plan, focus);
+    check_kset(plan, defocus);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    launch_mask_fft(plan->g, nullptr, mask_dev, plan->mhat.p, plan->scratch.p, nullptr, s);
+    ck_launch("mask fft");
+    forward(plan, focus, plan->If.p, nullptr, nullptr, s);
+    forward(plan, defocus, plan->Id.p, nullptr, nullptr, s);
+    ResistParams rp{i_th, sigma_z, 0.0, 0.0};
+    if (binarize)
+      launch_resist(plan->g, plan->If.p, plan->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, static_cast<uint8_t*>(nom), static_cast<uint8_t*>(inner), static_cast<uint8_t*>(outer),
+                    nullptr, nullptr, s);
+    else
+      launch_resist(plan->g, plan->If.p, plan->Id.p, nullptr, nullptr, rp, nullptr, nullptr,
+                    static_cast<double*>(nom), static_cast<double*>(inner), static_cast<double*>(outer), nullptr,
+                    nullptr, nullptr, nullptr, nullptr, s);
+    ck_launch("resist");
+  });
+}
+
+int lsopc_socs_gradient(lsopc_plan* plan, const lsopc_kset* ks, const double* mask_dev, const double* z_dev,
+                        const double* zt_dev, double sigma_z, double dose, double* out_dev, void* stream) {
+  return guarded([&] {
+    check_plan(plan);
+    check_kset(plan, ks);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t n = plan->n();
+    plan->A.ensure((size_t)ks->nk * n * plan->g.csize());
+    launch_mask_fft(plan->g, nullptr, mask_dev, plan->mhat.p, plan->scratch.p, nullptr, s);
+    ck_launch("mask fft");
+    forward(plan, ks, plan->If.p, plan->A.p, nullptr, s);
+    launch_gate(plan->g, z_dev, zt_dev, 1.0, plan->wf.p, s);
+    ck_launch("gate");
+    launch_adjoint_set(plan->g, ks->nk, plan->A.p, plan->wf.p, ks->spec.p, ks->w.data(), plan->G.p, true,
+                       plan->scratch.p, nullptr, s);
+    ck_launch("adjoint");
+    launch_adjoint_finish(plan->g, plan->G.p, 4.0 * sigma_z * dose / (double)n, out_dev, nullptr, nullptr,
+                          plan->scratch.p, nullptr, s);
+    ck_launch("adjoint finish");
+  });
+}
+
+int lsopc_convolve(lsopc_plan* plan, const lsopc_kset* ks, const double* mask_dev, double* out_c128_dev,
+                   void* stream) {
+  return guarded([&] {
+    check_plan(plan);
+    check_kset(plan, ks);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    plan->A.ensure((size_t)ks->nk * plan->n() * plan->g.csize());
+    launch_mask_fft(plan->g, nullptr, mask_dev, plan->mhat.p, plan->scratch.p, nullptr, s);
+    ck_launch("mask fft");
+    forward(plan, ks, plan->If.p, plan->A.p, nullptr, s);
+    launch_to_c128(plan->g, plan->A.p, out_c128_dev, s);
+    ck_launch("convert");
+  });
+}
+
+int lsopc_geometry_gradient(int H, int W, const double* phi, double* gx, double* gy, double* gxx, double* gyy,
+                            double* gxy, double* mag, void* stream) {
+  return guarded([&] {
+    if (H < 1 || W < 1) throw Error(LSOPC_EINVAL, "empty field");
+    launch_geometry(H, W, phi, gx, gy, gxx, gyy, gxy, mag, static_cast<cudaStream_t>(stream));
+    ck_launch("geometry");
+  });
+}
+
+int lsopc_curvature(int H, int W, const double* phi, const double* m, double weight, double* out, void* stream) {
+  return guarded([&] {
+    if (H < 1 || W < 1) throw Error(LSOPC_EINVAL, "empty field");
+    launch_curvature(H, W, phi, m, weight, out, static_cast<cudaStream_t>(stream));
+    ck_launch("curvature");
+  });
+}
+
+int lsopc_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_lower, double* phi, void* stream) {
+  return guarded([&] {
+    if (H < 1 || W < 1) throw Error(LSOPC_EINVAL, "empty mask");
+    if (!(d_lower < 0.0 && 0.0 < d_upper))
+      throw Error(LSOPC_EINVAL, "truncation bounds must satisfy D_l < 0 < D_u");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t n = (size_t)H * W;
+    DevBuf ones;
+    ones.ensure(n);
+    ck(cudaMemsetAsync(ones.p, 0, n, s), "memset");
+    double diff = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, mask, ones.as<uint8_t>(), nullptr, s);
+    ones.release();
+    if (diff == 0.0 || diff == (double)n) throw Error(LSOPC_EDEGENERATE, "mask is uniform: no boundary exists");
+    DevBuf si, sf;
+    si.ensure(tsdf_scratch_i32(H, W) * sizeof(int));
+    sf.ensure(tsdf_scratch_f64(H, W) * sizeof(double));
+    launch_tsdf(H, W, mask, d_upper, d_lower, phi, si.as<int>(), sf.as<double>(), s);
+    ck_launch("tsdf");
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int lsopc_elementwise(int op, size_t n, const double* a, const double* b, double p0, double p1, double p2,
+                      double* out, uint8_t* out8, void* stream) {
+  return guarded([&] {
+    if (op < EW_MASK || op > EW_HYPOT) throw Error(LSOPC_EINVAL, "unknown elementwise op");
+    if (n == 0) return;
+    launch_elementwise(op, n, a, b, p0, p1, p2, out, out8, static_cast<cudaStream_t>(stream));
+    ck_launch("elementwise");
+  });
+}
+
+int lsopc_reduce(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
+                 double* out_host, void* stream) {
+  return guarded([&] {
+    if (op < RD_SUMSQDIFF || op > RD_COUNTNEQ) throw Error(LSOPC_EINVAL, "unknown reduction");
+    if (n == 0) {
+      *out_host = 0.0;
+      return;
+    }
+    *out_host = reduce_to_host(op, n, a, b, a8, b8, nullptr, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"
+
+// ============================================================================
+// DSO loop session
+
+struct lsopc_session {
+  lsopc_plan* plan = nullptr;
+  const lsopc_kset* focus = nullptr;
+  const lsopc_kset* defocus = nullptr;
+  lsopc_config cfg{};
+  cudaStream_t s = nullptr;
+  DevBuf target, phi, best, v[2], d[2], u, mask, mod, hist, state, part_ls, part_up, dots, gm;
+  int it = 0;
+  bool have_mod = false;
+  ~lsopc_session() {
+    for (DevBuf* b : {&target, &phi, &best, &v[0], &v[1], &d[0], &d[1], &u, &mask, &mod, &hist, &state, &part_ls,
+                      &part_up, &dots, &gm})
+      b->release();
+  }
+  DevState* st() const { return state.as<DevState>(); }
+};
+
+namespace {
+
+void enqueue_iteration(lsopc_session* ss, int it) {
+  lsopc_plan* p = ss->plan;
+  const Grid& g = p->g;
+  const size_t n = g.n();
+  cudaStream_t s = ss->s;
+  DevState* st = ss->st();
+  StopFlag stop = &st->stopped;
+  const lsopc_config& c = ss->cfg;
+  double* v = ss->v[it & 1].as<double>();
+  double* vprev = ss->v[(it + 1) & 1].as<double>();
+  double* d = ss->d[it & 1].as<double>();
+  double* dprev = ss->d[(it + 1) & 1].as<double>();
+  const size_t fbytes = (size_t)ss->focus->nk * n * g.csize();
+  void* A_f = p->A.p;
+  void* A_d = static_cast<char*>(p->A.p) + fbytes;
+
+  // forward: M^ -> fields at the focus and defocus sets -> resist, losses, gates
+  launch_mask_fft(g, ss->mask.as<uint8_t>(), nullptr, p->mhat.p, p->scratch.p, stop, s);
+  forward(p, ss->focus, p->If.p, A_f, stop, s);
+  forward(p, ss->defocus, p->Id.p, A_d, stop, s);
+  ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
+  launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr, nullptr,
+                nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s);
+  LoopCfg lc{c.alpha, c.beta, c.stop_rel_tol, c.stop_patience};
+  launch_after_forward(p->partials.as<double>(), reduce_blocks(), lc, it, st, ss->hist.as<double>(), s);
+  launch_copy_best(n, ss->phi.as<double>(), ss->best.as<double>(), st, s);
+  // adjoint: one frequency-domain accumulator for both sets, one inverse
+  launch_adjoint_set(g, ss->focus->nk, A_f, p->wf.p, ss->focus->spec.p, ss->focus->w.data(), p->G.p, true,
+                     p->scratch.p, stop, s);
+  launch_adjoint_set(g, ss->defocus->nk, A_d, p->wd.p, ss->defocus->spec.p, ss->defocus->w.data(), p->G.p, false,
+                     p->scratch.p, stop, s);
+  int ndots = launch_adjoint_finish(g, p->G.p, 4.0 * c.sigma_z / (double)n, v, it > 0 ? vprev : nullptr,
+                                    ss->dots.as<double>(), p->scratch.p, stop, s);
+  const int restart = (it % c.cg_restart_every == 0) ? 1 : 0;
+  launch_after_grad(ss->dots.as<double>(), ndots, restart || it == 0, st, s);
+  // level-set step
+  launch_ls_velocity(g.H, g.W, ss->phi.as<double>(), v, dprev, ss->have_mod ? ss->mod.as<double>() : nullptr,
+                     c.curvature_weight, c.use_curvature, st, d, ss->u.as<double>(),
+                     c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), s);
+  launch_after_velocity(ss->part_ls.as<double>(), ls_blocks(), c.eta, st, ss->hist.as<double>(), s);
+  launch_ls_update(n, ss->phi.as<double>(), ss->u.as<double>(), c.update_form ? ss->gm.as<double>() : nullptr,
+                   c.d_lower, c.d_upper, st, ss->mask.as<uint8_t>(),
+                   ss->part_up.as<double>(), s);
+  launch_after_update(ss->part_up.as<double>(), ls_blocks(), st, ss->hist.as<double>(), s);
+  ck_launch("dso iteration");
+}
+
+}  // namespace
+
+extern "C" {
+
+int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_kset* defocus,
+                         const uint8_t* target_dev, const double* phi0_dev, const double* mod_dev,
+                         const lsopc_config* cfg, void* stream, lsopc_session** out) {
+  return guarded([&] {
+    check_plan(plan);
+    check_kset(plan, focus);
+    check_kset(plan, defocus);
+    if (!cfg || !out) throw Error(LSOPC_EINVAL, "null argument");
+    if (cfg->max_iters < 0) throw Error(LSOPC_EINVAL, "max_iters must be >= 0");
+    if (cfg->cg_restart_every < 1) throw Error(LSOPC_EINVAL, "cg_restart_every must be >= 1");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Grid& g = plan->g;
+    const size_t n = g.n();
+    auto* ss = new lsopc_session();
+    try {
+      ss->plan = plan;
+      ss->focus = focus;
+      ss->defocus = defocus;
+      ss->cfg = *cfg;
+      ss->s = s;
+      ss->target.ensure(n);
+      ck(cudaMemcpyAsync(ss->target.p, target_dev, n, cudaMemcpyDeviceToDevice, s), "memcpy");
+      ss->phi.ensure(n * 8);
+      ss->best.ensure(n * 8);
+      for (int i = 0; i < 2; ++i) {
+        ss->v[i].ensure(n * 8);
+        ss->d[i].ensure(n * 8);
+      }
+      ss->u.ensure(n * 8);
+      if (cfg->update_form) ss->gm.ensure(n * 8);
+      ss->mask.ensure(n);
+      ss->hist.ensure((size_t)(cfg->max_iters + 1) * 7 * sizeof(double));
+      ss->state.ensure(sizeof(DevState));
+      ss->part_ls.ensure((size_t)ls_blocks() * 2 * sizeof(double));
+      ss->part_up.ensure((size_t)ls_blocks() * sizeof(double));
+      ss->dots.ensure((size_t)g.H * 2 * sizeof(double));
+      plan->A.ensure((size_t)(focus->nk + defocus->nk) * n * g.csize());
+      // optimizer.py:197-201: uniform target -> DegenerateInputError
+      {
+        DevBuf zero;
+        zero.ensure(n);
+        ck(cudaMemsetAsync(zero.p, 0, n, s), "memset");
+        double lit = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, ss->target.as<uint8_t>(), zero.as<uint8_t>(),
+                                    plan, s);
+        zero.release();
+        if (lit == 0.0 || lit == (double)n) throw Error(LSOPC_EDEGENERATE, "target layout is uniform");
+      }
+      if (phi0_dev) {
+        ck(cudaMemcpyAsync(ss->phi.p, phi0_dev, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
+      } else {
+        plan->tsdf_i.ensure(tsdf_scratch_i32(g.H, g.W) * sizeof(int));
+        plan->tsdf_f.ensure(tsdf_scratch_f64(g.H, g.W) * sizeof(double));
+        launch_tsdf(g.H, g.W, ss->target.as<uint8_t>(), cfg->d_upper, cfg->d_lower, ss->phi.as<double>(),
+                    plan->tsdf_i.as<int>(), plan->tsdf_f.as<double>(), s);
+        ck_launch("tsdf");
+      }
+      if (mod_dev) {
+        ss->have_mod = true;
+        ss->mod.ensure(n * 8);
+        ck(cudaMemcpyAsync(ss->mod.p, mod_dev, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
+      }
+      ck(cudaMemcpyAsync(ss->best.p, ss->phi.p, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
+      launch_elementwise(EW_MASK, n, ss->phi.as<double>(), nullptr, 0, 0, 0, nullptr, ss->mask.as<uint8_t>(), s);
+      DevState h{};
+      h.best = std::numeric_limits<double>::infinity();
+      h.nonfinite_it = -1;
+      ck(cudaMemcpyAsync(ss->state.p, &h, sizeof(h), cudaMemcpyHostToDevice, s), "memcpy");
+      ck(cudaStreamSynchronize(s), "sync");
+    } catch (...) {
+      delete ss;
+      throw;
+    }
+    *out = ss;
+  });
+}
+
+int lsopc_session_enqueue(lsopc_session* ss, int n) {
+  return guarded([&] {
+    if (!ss) throw Error(LSOPC_EINVAL, "null session");
+    for (int i = 0; i < n && ss->it < ss->cfg.max_iters; ++i) enqueue_iteration(ss, ss->it++);
+  });
+}
+
+int lsopc_session_poll(lsopc_session* ss, int* stopped, int* iters_enqueued) {
+  return guarded([&] {
+    if (!ss) throw Error(LSOPC_EINVAL, "null session");
+    DevState h{};
+    ck(cudaMemcpyAsync(&h, ss->state.p, sizeof(h), cudaMemcpyDeviceToHost, ss->s), "memcpy");
+    ck(cudaStreamSynchronize(ss->s), "sync");
+    if (stopped) *stopped = h.stopped;
+    if (iters_enqueued) *iters_enqueued = ss->it;
+  });
+}
+
+int lsopc_session_finish(lsopc_session* ss, double* best_phi_dev, uint8_t* final_mask_dev, double* history_host,
+                         lsopc_result* res) {
+  return guarded([&] {
+    if (!ss) throw Error(LSOPC_EINVAL, "null session");
+    lsopc_plan* p = ss->plan;
+    const Grid& g = p->g;
+    const size_t n = g.n();
+    cudaStream_t s = ss->s;
+    DevState h{};
+    ck(cudaMemcpyAsync(&h, ss->state.p, sizeof(h), cudaMemcpyDeviceToHost, s), "memcpy");
+    ck(cudaStreamSynchronize(s), "sync");
+    if (h.nonfinite_it >= 0)
+      throw Error(LSOPC_ENUMERIC, "non-finite loss at iteration " + std::to_string(h.nonfinite_it));
+    if (history_host && h.nhist > 0)
+      ck(cudaMemcpy(history_host, ss->hist.p, (size_t)h.nhist * 7 * sizeof(double), cudaMemcpyDeviceToHost),
+         "memcpy");
+    // optimizer.py:271-277: best phi -> mask -> hard corners -> L2 / PVB
+    uint8_t* fm = final_mask_dev ? final_mask_dev : ss->mask.as<uint8_t>();
+    launch_elementwise(EW_MASK, n, ss->best.as<double>(), nullptr, 0, 0, 0, nullptr, fm, s);
+    launch_mask_fft(g, fm, nullptr, p->mhat.p, p->scratch.p, nullptr, s);
+    forward(p, ss->focus, p->If.p, nullptr, nullptr, s);
+    forward(p, ss->defocus, p->Id.p, nullptr, nullptr, s);
+    uint8_t* hn = p->hard.as<uint8_t>();
+    ResistParams rp{ss->cfg.i_th, ss->cfg.sigma_z, 0.0, 0.0};
+    launch_resist(g, p->If.p, p->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr, nullptr, hn, hn + n,
+                  hn + 2 * n, nullptr, nullptr, s);
+    ck_launch("final prints");
+    double l2 = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn, ss->target.as<uint8_t>(), p, s);
+    double pvb = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn + n, hn + 2 * n, p, s);
+    if (best_phi_dev) ck(cudaMemcpyAsync(best_phi_dev, ss->best.p, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
+    ck(cudaStreamSynchronize(s), "sync");
+    if (res) {
+      res->iters = h.nhist;
+      res->l2 = (int)l2;
+      res->pvband = (int)pvb;
+      res->nonfinite_iter = h.nonfinite_it;
+    }
+  });
+}
+
+int lsopc_session_phi(lsopc_session* ss, double* phi_dev) {
+  return guarded([&] {
+    if (!ss) throw Error(LSOPC_EINVAL, "null session");
+    ck(cudaMemcpyAsync(phi_dev, ss->phi.p, ss->plan->n() * 8, cudaMemcpyDeviceToDevice, ss->s), "memcpy");
+  });
+}
+
+int lsopc_session_destroy(lsopc_session* ss) {
+  return guarded([&] {
+    if (ss) cudaStreamSynchronize(ss->s);
+    delete ss;
+  });
+}
+
+int lsopc_session_launches_per_iter(const lsopc_session* ss) {
+  if (!ss) return 0;
+  // mask fft 2, forward 2 per kernel, resist+after 2, copy 1, adjoint 2 per kernel,
+  // finish 2, after_grad 1, velocity+after 2, update+after 2
+  const int nk = ss->focus->nk + ss->defocus->nk;
+  return 2 + 2 * nk + 2 + 1 + 2 * nk + 2 + 1 + 2 + 2;
+}
+
+int lsopc_optimize(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_kset* defocus, const uint8_t* target_dev,
+                   const double* phi0_dev, const double* mod_dev, const lsopc_config* cfg, double* best_phi_dev,
+                   uint8_t* final_mask_dev, double* history_host, lsopc_result* result, void* stream) {
+  lsopc_session* ss = nullptr;
+  int rc = lsopc_session_create(plan, focus, defocus, target_dev, phi0_dev, mod_dev, cfg, stream, &ss);
+  if (rc) return rc;
+  int chunk = 2;
+  while (true) {
+    rc = lsopc_session_enqueue(ss, chunk);
+    if (rc) break;
+    int stopped = 0, enq = 0;
+    rc = lsopc_session_poll(ss, &stopped, &enq);
+    if (rc || stopped || enq >= cfg->max_iters) break;
+    if (chunk < 8) chunk *= 2;
+  }
+  if (!rc) rc = lsopc_session_finish(ss, best_phi_dev, final_mask_dev, history_host, result);
+  std::string keep = g_err;
+  lsopc_session_destroy(ss);
+  g_err = keep;
+  return rc;
+}
+
+// metrics.py:55-87 _largest_rect: histogram stack sweep, ties topmost then leftmost
+static void largest_rect(const std::vector<uint8_t>& m, int H, int W, std::vector<long long>& heights,
+                         std::vector<int>& stack, long long& best, int& bx, int& by, int& bw, int& bh) {
+  std::fill(heights.begin(), heights.end(), 0);
+  best = 0;
+  bx = by = bw = bh = 0;
+  for (int y = 0; y < H; ++y) {
+    const uint8_t* row = &m[(size_t)y * W];
+    for (int x = 0; x < W; ++x) heights[x] = row[x] ? heights[x] + 1 : 0;
+    int top = -1;
+    for (int x = 0; x <= W; ++x) {
+      long long cur = x < W ? heights[x] : 0;
+      while (top >= 0 && heights[stack[top]] > cur) {
+        long long hh = heights[stack[top]];
+        --top;
+        int left = top >= 0 ? stack[top] + 1 : 0;
+        int width = x - left;
+        long long area = hh * width;
+        int ty = y - (int)hh + 1;
+        if (area > best || (area == best && (ty < by || (ty == by && left < bx)))) {
+          best = area;
+          bx = left;
+          by = ty;
+          bw = width;
+          bh = (int)hh;
+        }
+      }
+      stack[++top] = x;
+    }
+  }
+}
+
+int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* rects, size_t cap, size_t* count) {
+  return guarded([&] {
+    std::vector<uint8_t> work((size_t)H * W);
+    for (size_t i = 0; i < work.size(); ++i) work[i] = mask_host[i] != 0;
+    std::vector<long long> heights(W);
+    std::vector<int> stack(W + 1);
+    size_t k = 0;
+    while (true) {
+      long long area;
+      int x, y, w, h;
+      largest_rect(work, H, W, heights, stack, area, x, y, w, h);
+      if (area == 0) break;
+      if (rects && k < cap) {
+        rects[4 * k] = x;
+        rects[4 * k + 1] = y;
+        rects[4 * k + 2] = w;
+        rects[4 * k + 3] = h;
+      }
+      ++k;
+      for (int yy = y; yy < y + h; ++yy) std::memset(&work[(size_t)yy * W + x], 0, w);
+    }
+    *count = k;
+  });
+}
+
+}  // extern "C"

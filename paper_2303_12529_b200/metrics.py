@@ -1,0 +1,78 @@
+"""Mask metrics: drop-in for the reference `lsopc.metrics` (metrics.py:1-108).
+
+L2 / PVBand are device popcounts; the greedy fracturing shot count is native
+host code in the same library (lsopc_fracture).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nv
+
+__all__ = ["MetricsReport", "l2_error", "pvband", "fracture", "shot_count"]
+
+
+@dataclass
+class MetricsReport:
+    l2: int
+    pvband: int
+    shots: int
+    wall_time: float = 0.0
+    iters: int = 0
+
+    def as_dict(self):
+        return {"l2": int(self.l2), "pvband": int(self.pvband), "shots": int(self.shots),
+                "wall_time_s": float(self.wall_time), "iters": int(self.iters)}
+
+
+def _count_neq(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if a.shape != b.shape:
+        raise ValueError(f"dimension mismatch: {a.shape} vs {b.shape}")
+    if a.size == 0:
+        return 0
+    return int(nv.reduce("countneq", a.size, nv.to_dev(a.ravel()), nv.to_dev(b.ravel())))
+
+
+def l2_error(z, z_t, pitch=1):
+    """Disagreeing pixels times pitch^2 (metrics.py:39-44)."""
+    return _count_neq(z, z_t) * pitch * pitch
+
+
+def pvband(z_in, z_out, pitch=1):
+    """XOR area of the inner and outer prints times pitch^2 (metrics.py:47-52)."""
+    return _count_neq(z_in, z_out) * pitch * pitch
+
+
+def fracture(mask):
+    """Greedy largest-rectangle decomposition, ties topmost then leftmost
+    (metrics.py:55-104).  Returns [(x, y, w, h), ...]."""
+    m = np.ascontiguousarray((np.asarray(mask) != 0).astype(np.uint8))
+    if m.ndim != 2:
+        raise ValueError("mask must be 2-D")
+    H, W = m.shape
+    if m.size == 0:
+        return []
+    count = ctypes.c_size_t()
+    nv.check(nv.lib().lsopc_fracture(H, W, m.ctypes.data_as(ctypes.c_void_p), None, 0,
+                                     ctypes.byref(count)))
+    buf = np.empty((max(count.value, 1), 4), dtype=np.int32)
+    nv.check(nv.lib().lsopc_fracture(H, W, m.ctypes.data_as(ctypes.c_void_p),
+                                     buf.ctypes.data_as(ctypes.c_void_p), count.value,
+                                     ctypes.byref(count)))
+    return [tuple(int(v) for v in r) for r in buf[:count.value]]
+
+
+def shot_count(mask):
+    m = np.ascontiguousarray((np.asarray(mask) != 0).astype(np.uint8))
+    if m.size == 0:
+        return 0
+    count = ctypes.c_size_t()
+    nv.check(nv.lib().lsopc_fracture(m.shape[0], m.shape[1], m.ctypes.data_as(ctypes.c_void_p),
+                                     None, 0, ctypes.byref(count)))
+    return int(count.value)

@@ -1,0 +1,348 @@
+"""The DSO level-set ILT loop: drop-in for the reference `lsopc.optimizer`
+(optimizer.py:1-341).
+
+`optimize` runs the whole loop on the device through the C ABI
+(`lsopc_optimize`): forward, losses, best iterate, adjoint, CG, CFL and the
+level-set update are sm_100a kernels and the stop rule is evaluated on the
+device, so the host only enqueues iterations and polls a flag.  The
+operator-level functions (losses, gradients, CG, CFL, motion term) are the
+same kernels exposed one call at a time.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nv
+from . import litho
+from .errors import DegenerateInputError
+from .levelset import LevelSetField, heaviside, mask_from_phi
+from .metrics import MetricsReport, shot_count
+
+_EPS_GRAD = 1e-8
+
+__all__ = [
+    "OptConfig", "IterationRecord", "OptimizationResult",
+    "ilt_loss", "pvb_loss", "ilt_gradient", "pvb_gradient",
+    "velocity", "motion_term", "cfl_timestep", "cg_direction",
+    "optimize", "modulation_search", "ModulationSearchResult",
+]
+
+
+@dataclass
+class OptConfig:
+    """Reference hyper-parameters and defaults (optimizer.py:38-64), plus
+    `precision` ("fp64" | "fp32" | None = package default) selecting the
+    transform tier.  epsilon and grid_side are accepted and inert, as in the
+    reference."""
+    alpha: float = 1.0
+    beta: float = 7.5
+    curvature_weight: float = 0.9
+    sigma_z: float = 50.0
+    i_th: float = 0.225
+    epsilon: float = 0.03
+    eta: float = 0.85
+    d_upper: float = 900.0
+    d_lower: float = -100.0
+    max_iters: int = 100
+    stop_rel_tol: float = 1e-4
+    stop_patience: int = 5
+    use_curvature: bool = True
+    grid_side: int = 0
+    cg_restart_every: int = 50
+    precision: str = None
+
+    def __post_init__(self):
+        if self.alpha < 0 or self.beta < 0 or (self.alpha == 0 and self.beta == 0):
+            raise ValueError("alpha, beta must be >= 0 and not both zero")
+        if not 0 < self.eta <= 1:
+            raise ValueError("eta must be in (0, 1]")
+        if self.sigma_z <= 0:
+            raise ValueError("sigma_z must be positive")
+        if self.max_iters < 0:
+            raise ValueError("max_iters must be >= 0")
+        if self.precision is not None and str(self.precision).lower() not in ("fp32", "fp64"):
+            raise ValueError("precision must be fp32, fp64 or None")
+
+
+@dataclass
+class IterationRecord:
+    l_ilt: float
+    l_pvb: float
+    l_dso: float
+    dt: float
+    max_v: float
+    max_step: float
+    max_grad_mag: float
+
+
+@dataclass
+class OptimizationResult:
+    final_mask: np.ndarray
+    final_phi: LevelSetField
+    metrics: MetricsReport
+    loss_history: list
+    iters_run: int
+    wall_time: float
+
+
+# ---------------------------------------------------------------------------
+# operator-level API
+
+
+def _f64(a):
+    return np.asarray(a, dtype=np.float64)
+
+
+def _bcast_pair(a, b):
+    a, b = np.broadcast_arrays(_f64(a), _f64(b))
+    return np.ascontiguousarray(a), np.ascontiguousarray(b)
+
+
+def ilt_loss(z, z_t):
+    """sum (Z - Z_t)^2 (optimizer.py:88-90), deterministic device reduction."""
+    a, b = _bcast_pair(z, z_t)
+    if a.size == 0:
+        return 0.0
+    return float(nv.reduce("sumsqdiff", a.size, nv.to_dev(a), nv.to_dev(b)))
+
+
+def pvb_loss(z_in, z_out, z_t):
+    """sum (Z_in - Z_t)^2 + sum (Z_out - Z_t)^2 (optimizer.py:93-96)."""
+    return float(ilt_loss(z_in, z_t) + ilt_loss(z_out, z_t))
+
+
+def _socs_gradient_dev(mask, z, z_t, kernels, sigma_z, dose):
+    m = _f64(mask)
+    dks = kernels.device(m.shape)
+    zz, zt = _bcast_pair(z, z_t)
+    out = nv.empty(m.shape, np.float64)
+    md, zd, ztd = nv.to_dev(m), nv.to_dev(zz), nv.to_dev(zt)
+    nv.check(nv.lib().lsopc_socs_gradient(dks.plan.handle, dks.handle, nv.ptr(md), nv.ptr(zd),
+                                          nv.ptr(ztd), float(sigma_z), float(dose), nv.ptr(out),
+                                          nv.stream()))
+    return out
+
+
+def _socs_gradient(mask, z, z_t, kernels, sigma_z, dose):
+    """d sum (Z - Z_t)^2 / dM through the sigmoid and SOCS model
+    (optimizer.py:99-111)."""
+    return nv.to_host(_socs_gradient_dev(mask, z, z_t, kernels, sigma_z, dose))
+
+
+def ilt_gradient(mask, z, z_t, kernels, cfg):
+    """Nominal-corner loss gradient (optimizer.py:114-119)."""
+    if kernels.side > min(np.shape(mask)):
+        raise ValueError("kernel side exceeds grid")
+    return _socs_gradient(mask, z, z_t, kernels, cfg.sigma_z, dose=1.0)
+
+
+def pvb_gradient(mask, z_in, z_out, z_t, focus_kernels, defocus_kernels, cfg):
+    """Inner (defocus, 0.98) + outer (focus, 1.02) gradients (optimizer.py:122-129)."""
+    gi = _socs_gradient_dev(mask, z_in, z_t, defocus_kernels, cfg.sigma_z, litho.INNER.dose)
+    go = _socs_gradient_dev(mask, z_out, z_t, focus_kernels, cfg.sigma_z, litho.OUTER.dose)
+    out = nv.empty(gi.shape, np.float64)
+    nv.elementwise("axpby", gi.numel(), gi, go, 1.0, 1.0, out=out)
+    return nv.to_host(out)
+
+
+def velocity(g_ilt, g_pvb, cfg):
+    """alpha g_ilt + beta g_pvb (optimizer.py:132-134)."""
+    a, b = _bcast_pair(g_ilt, g_pvb)
+    out = nv.empty(a.shape, np.float64)
+    if a.size:
+        nv.elementwise("axpby", a.size, nv.to_dev(a), nv.to_dev(b), float(cfg.alpha),
+                       float(cfg.beta), out=out)
+    return nv.to_host(out)
+
+
+def motion_term(v, phi, kappa=0.0):
+    """-v |grad phi| + kappa (optimizer.py:137-140)."""
+    from .levelset import gradient_magnitude
+    gm = gradient_magnitude(phi)
+    vv = np.ascontiguousarray(np.broadcast_to(_f64(v), gm.shape))
+    out = nv.empty(gm.shape, np.float64)
+    nv.elementwise("motion", gm.size, nv.to_dev(vv), nv.to_dev(gm), out=out)
+    kk = np.ascontiguousarray(np.broadcast_to(_f64(kappa), gm.shape))
+    res = nv.empty(gm.shape, np.float64)
+    nv.elementwise("axpby", gm.size, out, nv.to_dev(kk), 1.0, 1.0, out=res)
+    return nv.to_host(res)
+
+
+def cfl_timestep(v_effective, eta):
+    """(eta / max|v|, False), or (0, True) for a zero field (optimizer.py:143-151)."""
+    a = np.ascontiguousarray(_f64(v_effective))
+    vmax = float(nv.reduce("maxabs", a.size, nv.to_dev(a))) if a.size else 0.0
+    if vmax == 0.0:
+        return 0.0, True
+    return eta / vmax, False
+
+
+def cg_direction(g, g_prev=None, d_prev=None):
+    """Polak-Ribiere+ direction with restart (optimizer.py:154-169)."""
+    gg = np.ascontiguousarray(_f64(g))
+    gd = nv.to_dev(gg)
+    out = nv.empty(gg.shape, np.float64)
+    beta = None
+    if g_prev is not None and d_prev is not None and gg.size:
+        gp = nv.to_dev(np.broadcast_to(_f64(g_prev), gg.shape))
+        den = float(nv.reduce("dot", gg.size, gp, gp))
+        if den != 0.0:
+            b = float(nv.reduce("dotdiff", gg.size, gd, gp)) / den
+            if b > 0.0:
+                beta = b
+    if beta is None:
+        nv.elementwise("neg", gg.size, gd, out=out)
+    else:
+        dp = nv.to_dev(np.broadcast_to(_f64(d_prev), gg.shape))
+        nv.elementwise("cg", gg.size, gd, dp, beta, out=out)
+    return nv.to_host(out)
+
+
+def _forward_losses(mask, target, focus_kernels, defocus_kernels, cfg):
+    """optimizer.py:172-177."""
+    prints = litho.print_corners(mask, focus_kernels, defocus_kernels, cfg, binarize=False)
+    l_ilt = ilt_loss(prints.nominal, target)
+    l_pvb = pvb_loss(prints.inner, prints.outer, target)
+    return prints, l_ilt, l_pvb, cfg.alpha * l_ilt + cfg.beta * l_pvb
+
+
+def _check_target(target):
+    t = (np.asarray(target) != 0).astype(np.uint8)
+    if t.all() or not t.any():
+        raise DegenerateInputError("target layout is uniform")
+    return t
+
+
+# ---------------------------------------------------------------------------
+# the loop
+
+
+def _native_cfg(cfg, max_iters=None, stop_patience=None, use_curvature=None, update_form=0):
+    c = nv.LsopcConfig()
+    c.alpha, c.beta = float(cfg.alpha), float(cfg.beta)
+    c.curvature_weight, c.sigma_z = float(cfg.curvature_weight), float(cfg.sigma_z)
+    c.i_th, c.eta = float(cfg.i_th), float(cfg.eta)
+    c.d_upper, c.d_lower = float(cfg.d_upper), float(cfg.d_lower)
+    c.max_iters = int(cfg.max_iters if max_iters is None else max_iters)
+    c.stop_rel_tol = float(cfg.stop_rel_tol)
+    c.stop_patience = int(min(cfg.stop_patience if stop_patience is None else stop_patience, 2**31 - 1))
+    c.use_curvature = int(bool(cfg.use_curvature if use_curvature is None else use_curvature))
+    c.cg_restart_every = int(cfg.cg_restart_every)
+    c.update_form = int(update_form)
+    return c
+
+
+def _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation):
+    target = _check_target(target)
+    shape = target.shape
+    if phi0 is not None and phi0.shape != shape:
+        raise ValueError("phi0 dimensions do not match target")
+    m = None
+    if modulation is not None:
+        m = _f64(modulation)
+        if m.shape != shape:
+            raise ValueError("modulation dimensions do not match target")
+        if m.size and (m.min() < 0 or m.max() > 1):
+            raise ValueError("modulation values must lie in [0, 1]")
+    for ks, sel in ((focus_kernels, "focus"), (defocus_kernels, "defocus")):
+        if ks.side > min(shape):
+            raise ValueError(f"kernel side {ks.side} exceeds grid {shape}")
+        if ks.condition != sel:
+            raise ValueError(f"kernel set condition {ks.condition!r} does not match "
+                             f"process condition {sel!r}")
+    prec = cfg.precision
+    fk = focus_kernels.device(shape, prec)
+    dk = defocus_kernels.device(shape, prec)
+    return target, m, fk, dk
+
+
+def optimize(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=None):
+    """Full level-set ILT loop on the device (optimizer.py:204-284).  Returns
+    the lowest-loss iterate, binarised, with hard-resist metrics and the loss
+    history."""
+    t0 = time.perf_counter()
+    target, m, fk, dk = _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
+    shape = target.shape
+    td = nv.to_dev(target, np.uint8)
+    p0 = nv.to_dev(phi0.phi) if phi0 is not None else None
+    mdv = nv.to_dev(m) if m is not None else None
+    best = nv.empty(shape, np.float64)
+    fmask = nv.empty(shape, np.uint8)
+    hist = np.zeros((cfg.max_iters + 1, 7))
+    res = nv.LsopcResult()
+    c = _native_cfg(cfg)
+    nv.check(nv.lib().lsopc_optimize(fk.plan.handle, fk.handle, dk.handle, nv.ptr(td), nv.ptr(p0),
+                                     nv.ptr(mdv), ctypes.byref(c), nv.ptr(best), nv.ptr(fmask),
+                                     hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res),
+                                     nv.stream()))
+    final_mask = nv.to_host(fmask)
+    best_phi = nv.to_host(best)
+    wall = time.perf_counter() - t0
+    history = [IterationRecord(*(float(v) for v in row)) for row in hist[:res.iters]]
+    bounds = (cfg.d_upper, cfg.d_lower)
+    if phi0 is not None:
+        # the initial iterate keeps phi0's own bounds (optimizer.py:219-220,231);
+        # the best iterate is the first strict minimum of the recorded losses
+        losses = [h.l_dso for h in history]
+        if not losses or int(np.argmin(losses)) == 0:
+            bounds = (phi0.d_upper, phi0.d_lower)
+    report = MetricsReport(l2=res.l2, pvband=res.pvband, shots=shot_count(final_mask),
+                           wall_time=wall, iters=res.iters)
+    return OptimizationResult(final_mask=final_mask,
+                              final_phi=LevelSetField(best_phi, bounds[0], bounds[1]),
+                              metrics=report, loss_history=history, iters_run=res.iters,
+                              wall_time=wall)
+
+
+@dataclass
+class ModulationSearchResult:
+    m_gt: np.ndarray
+    best_delta_h: float
+    candidates: list = field(default_factory=list)
+
+
+def modulation_search(phi_gt, target, focus_kernels, defocus_kernels, cfg, num_samples=41,
+                      eval_steps=10):
+    """Exhaustive curvature-gate search (optimizer.py:294-341): each candidate
+    gate H(phi_gt + dh) is scored by L_DSO after `eval_steps` device
+    iterations with curvature on; ties break on smallest |dh|, then dh."""
+    if num_samples < 1:
+        raise ValueError("num_samples must be >= 1")
+    target = _check_target(target)
+    offsets = [0.0] if num_samples == 1 else list(np.linspace(-20.0, 20.0, num_samples))
+    eval_cfg = OptConfig(**{**cfg.__dict__, "use_curvature": True})
+    _, _, fk, dk = _prepare(target, focus_kernels, defocus_kernels, eval_cfg, phi_gt, None)
+    shape = target.shape
+    td = nv.to_dev(target, np.uint8)
+    pd = nv.to_dev(phi_gt.phi)
+    c = _native_cfg(eval_cfg, max_iters=eval_steps, stop_patience=2**31 - 1, use_curvature=True,
+                    update_form=1)
+    candidates, gates = [], {}
+    phi_out = nv.empty(shape, np.float64)
+    for dh in offsets:
+        gate = heaviside(phi_gt.phi + dh).astype(np.float64)
+        gates[dh] = gate
+        sess = ctypes.c_void_p()
+        nv.check(nv.lib().lsopc_session_create(fk.plan.handle, fk.handle, dk.handle, nv.ptr(td),
+                                               nv.ptr(pd), nv.ptr(nv.to_dev(gate)), ctypes.byref(c),
+                                               nv.stream(), ctypes.byref(sess)))
+        try:
+            nv.check(nv.lib().lsopc_session_enqueue(sess, eval_steps))
+            nv.check(nv.lib().lsopc_session_phi(sess, nv.ptr(phi_out)))
+            stopped = ctypes.c_int()
+            nv.check(nv.lib().lsopc_session_poll(sess, ctypes.byref(stopped), None))
+        finally:
+            nv.lib().lsopc_session_destroy(sess)
+        mask = mask_from_phi(nv.to_host(phi_out)).astype(np.float64)
+        _, _, _, l_final = _forward_losses(mask, target, focus_kernels, defocus_kernels, eval_cfg)
+        candidates.append((dh, l_final))
+    best_loss = min(l for _, l in candidates)
+    tied = [dh for dh, l in candidates if l == best_loss]
+    best_dh = min(tied, key=lambda d: (abs(d), d))
+    return ModulationSearchResult(gates[best_dh], best_dh, candidates)

@@ -1,0 +1,406 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the numpy oracle
+and the reference's golden vectors.  Marked `gpu`.
+
+Tolerances: FP64 tier -- the reference's own bars (1e-8 .. 1e-12 relative,
+bit-exact stencils/TSDF); FP32 tier -- the north-star bar of <= 1e-4 relative
+on intensity, loss and gradient (we assert 1e-5 / 2e-5).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import lsopc_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+b2 = pytest.importorskip("paper_2303_12529_b200")
+from paper_2303_12529_b200 import _native as nv  # noqa: E402
+
+
+@pytest.fixture(params=["fp64", "fp32"])
+def prec(request):
+    old = nv.get_precision()
+    nv.set_precision(request.param)
+    yield request.param
+    nv.set_precision(old)
+
+
+def ks_from(arrs, cond):
+    c, w = arrs
+    return b2.KernelSet([b2.OpticalKernel(ci, float(wi)) for ci, wi in zip(c, w)], cond)
+
+
+def kernels(side, n_k, seed):
+    f, d = o.synthetic_kernels(side, n_k, seed)
+    return f, d, ks_from(f, "focus"), ks_from(d, "defocus")
+
+
+def relerr(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300)
+
+
+TOL = {"fp64": 1e-12, "fp32": 1e-5}
+
+
+# ---------------------------------------------------------------------------
+# forward model
+
+@pytest.mark.parametrize("shape", [(8, 8), (16, 16), (32, 32), (64, 64), (128, 64), (64, 256),
+                                   (256, 256), (512, 512), (1024, 1024)])
+def test_aerial_intensity_vs_oracle(prec, shape):
+    rng = np.random.default_rng(sum(shape))
+    k = min(7, min(shape) - 1) | 1
+    f, d, F, D = kernels(k, 3, 2)
+    m = (rng.random(shape) < 0.4).astype(np.float64)
+    for arrs, ks, cond in ((f, F, b2.NOMINAL), (f, F, b2.OUTER), (d, D, b2.INNER)):
+        out = b2.aerial_intensity(m, ks, cond)
+        ref = o.intensity(m, arrs[0], arrs[1], cond.dose)
+        assert out.shape == shape
+        assert relerr(out, ref) <= TOL[prec]
+        assert out.min() >= 0.0
+
+
+def test_aerial_intensity_golden(prec):
+    g = golden("forward")
+    kg = golden("kernels")
+    F = ks_from((kg["9_2_3_f_c"], kg["9_2_3_f_w"]), "focus")
+    D = ks_from((kg["9_2_3_d_c"], kg["9_2_3_d_w"]), "defocus")
+    m = g["rand64_mask"]
+    for key, ks, cond in (("I_nom", F, b2.NOMINAL), ("I_out", F, b2.OUTER), ("I_in", D, b2.INNER)):
+        assert relerr(b2.aerial_intensity(m, ks, cond), g[f"rand64_{key}"]) <= TOL[prec]
+
+
+def test_delta_kernel_identity():
+    rng = np.random.default_rng(12345)
+    mask = (rng.random((16, 16)) < 0.5).astype(np.float64)
+    c = np.zeros((5, 5), dtype=np.complex128)
+    c[2, 2] = 1.0
+    ks = b2.KernelSet([b2.OpticalKernel(c, 1.0)], "focus")
+    assert np.allclose(b2.aerial_intensity(mask, ks, b2.NOMINAL), mask, atol=1e-12)
+
+
+def test_spatial_convolution_oracle():
+    """fields.convolve against a tap-by-tap periodic sum (conftest-style)."""
+    rng = np.random.default_rng(3)
+    mask = rng.random((64, 64))
+    f, d, F, D = kernels(9, 3, 5)
+    for coeffs in list(f[0]) + list(d[0]):
+        out = b2.convolve(mask, coeffs)
+        ref = np.zeros(mask.shape, dtype=np.complex128)
+        K = coeffs.shape[0]
+        for i in range(K):
+            for j in range(K):
+                ref += coeffs[i, j] * np.roll(mask, (i - K // 2, j - K // 2), axis=(0, 1))
+        assert np.abs(out - ref).max() <= 1e-9 * np.abs(ref).max()
+
+
+def test_convolve_wraparound_small_grid():
+    mask = np.zeros((8, 8))
+    mask[0, 0] = 1.0
+    out = b2.convolve(mask, np.ones((3, 3), dtype=np.complex128)).real
+    exp = np.zeros((8, 8))
+    for y in (-1, 0, 1):
+        for x in (-1, 0, 1):
+            exp[y % 8, x % 8] = 1.0
+    assert np.allclose(out, exp, atol=1e-10)
+
+
+def test_print_corners_golden(prec):
+    g = golden("forward")
+    kg = golden("kernels")
+    F = ks_from((kg["9_2_3_f_c"], kg["9_2_3_f_w"]), "focus")
+    D = ks_from((kg["9_2_3_d_c"], kg["9_2_3_d_w"]), "defocus")
+    soft = b2.print_corners(g["bin32_mask"], F, D, b2.OptConfig(), binarize=False)
+    hard = b2.print_corners(g["bin32_mask"], F, D, b2.OptConfig(), binarize=True)
+    tol = 1e-12 if prec == "fp64" else 1e-5
+    for c, key in (("nominal", "nom"), ("inner", "in"), ("outer", "out")):
+        assert np.abs(getattr(soft, c) - g[f"bin32_Z_{key}"]).max() <= tol
+        assert np.array_equal(getattr(hard, c), g[f"bin32_H_{key}"])
+
+
+def test_condition_and_size_validation():
+    f, d, F, D = kernels(9, 1, 0)
+    with pytest.raises(ValueError):
+        b2.aerial_intensity(np.zeros((16, 16)), D, b2.NOMINAL)
+    with pytest.raises(ValueError):
+        b2.aerial_intensity(np.zeros((8, 8)), F, b2.NOMINAL)
+    with pytest.raises(ValueError):
+        b2.aerial_intensity(np.zeros((24, 24)), F, b2.NOMINAL)  # not a power of two
+
+
+# ---------------------------------------------------------------------------
+# gradients
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_gradients_golden(prec, seed):
+    g = golden("gradients")
+    kg = golden("kernels")
+    F = ks_from((kg[f"9_2_{seed}_f_c"], kg[f"9_2_{seed}_f_w"]), "focus")
+    D = ks_from((kg[f"9_2_{seed}_d_c"], kg[f"9_2_{seed}_d_w"]), "defocus")
+    target = g[f"s{seed}_target"]
+    mask = target.astype(np.float64)
+    cfg = b2.OptConfig()
+    p = b2.print_corners(mask, F, D, cfg, binarize=False)
+    gi = b2.ilt_gradient(mask, p.nominal, target, F, cfg)
+    gp = b2.pvb_gradient(mask, p.inner, p.outer, target, F, D, cfg)
+    tol = 1e-10 if prec == "fp64" else 2e-5
+    assert relerr(gi, g[f"s{seed}_g_ilt"]) <= tol
+    assert relerr(gp, g[f"s{seed}_g_pvb"]) <= tol
+    ltol = 1e-12 if prec == "fp64" else 1e-6
+    assert abs(b2.ilt_loss(p.nominal, target) - g[f"s{seed}_l_ilt"]) <= ltol * g[f"s{seed}_l_ilt"]
+    assert abs(b2.pvb_loss(p.inner, p.outer, target) - g[f"s{seed}_l_pvb"]) <= ltol * g[f"s{seed}_l_pvb"]
+
+
+def test_gradient_finite_differences_fp64():
+    """AC-1 style: central differences of the device forward model pin the
+    device adjoint (rel 1e-3 / abs 1e-6)."""
+    nv.set_precision("fp64")
+    f, d, F, D = kernels(9, 2, 0)
+    target = np.zeros((64, 64), dtype=np.uint8)
+    target[16:48, 22:42] = 1
+    mask = target.astype(np.float64)
+    cfg = b2.OptConfig()
+    p = b2.print_corners(mask, F, D, cfg, binarize=False)
+    gi = b2.ilt_gradient(mask, p.nominal, target, F, cfg)
+    gp = b2.pvb_gradient(mask, p.inner, p.outer, target, F, D, cfg)
+    rng = np.random.default_rng(42)
+    h = 1e-3
+    for _ in range(12):
+        y, x = rng.integers(0, 64, size=2)
+        mp, mm = mask.copy(), mask.copy()
+        mp[y, x] += h
+        mm[y, x] -= h
+        pp = b2.print_corners(mp, F, D, cfg, binarize=False)
+        pm = b2.print_corners(mm, F, D, cfg, binarize=False)
+        fd_i = (b2.ilt_loss(pp.nominal, target) - b2.ilt_loss(pm.nominal, target)) / (2 * h)
+        fd_p = (b2.pvb_loss(pp.inner, pp.outer, target) - b2.pvb_loss(pm.inner, pm.outer, target)) / (2 * h)
+        for an, fd in ((gi[y, x], fd_i), (gp[y, x], fd_p)):
+            if abs(an) < 1e-9:
+                assert abs(fd - an) <= 1e-6
+            else:
+                assert abs(fd - an) <= 1e-3 * abs(an)
+
+
+def test_gradient_linear_in_residual():
+    nv.set_precision("fp64")
+    f, d, F, D = kernels(9, 2, 5)
+    target = np.zeros((64, 64), dtype=np.uint8)
+    target[16:48, 21:42] = 1
+    mask = target.astype(np.float64)
+    cfg = b2.OptConfig()
+    z = b2.print_corners(mask, F, D, cfg, binarize=False).nominal
+    delta = z - target
+    g1 = b2.ilt_gradient(mask, z, z - delta, F, cfg)
+    g3 = b2.ilt_gradient(mask, z, z - 3.0 * delta, F, cfg)
+    assert np.allclose(g3, 3.0 * g1, rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# level set (bit-exact float64)
+
+def test_geometry_curvature_bit_exact():
+    g = golden("levelset")
+    gg = b2.geometry_gradient(g["phi"])
+    for name in ("gx", "gy", "gxx", "gyy", "gxy"):
+        assert np.array_equal(getattr(gg, name), g[name]), name
+    assert np.array_equal(gg.magnitude, g["mag"])
+    assert np.array_equal(b2.curvature(g["phi"], g["mod"], 0.9), g["kappa"])
+
+
+def test_hypot_matches_numpy_bitwise():
+    rng = np.random.default_rng(0)
+    n = 1 << 20
+    a = rng.standard_normal(n) * 10.0 ** rng.integers(-6, 5, n)
+    b = rng.standard_normal(n) * 10.0 ** rng.integers(-6, 5, n)
+    b[:1000] = 0.0
+    gg = b2.levelset.GeometryGradient(a.reshape(1024, 1024), b.reshape(1024, 1024), None, None, None)
+    assert np.array_equal(gg.magnitude, np.hypot(a, b).reshape(1024, 1024))
+
+
+def test_tsdf_bit_exact_golden():
+    g = golden("levelset")
+    for i in range(4):
+        assert np.array_equal(b2.tsdf_from_mask(g[f"tsdf_mask{i}"]).phi, g[f"tsdf_phi{i}"])
+    t = o.rect_layout(128, [(25, 30, 30, 50), (70, 60, 40, 40)])
+    assert np.array_equal(b2.tsdf_from_mask(t, 20.0, -7.0).phi, g["tsdf_two_rect"])
+
+
+@pytest.mark.parametrize("shape", [(7, 13), (64, 64), (100, 37), (512, 512)])
+def test_tsdf_random_vs_oracle(shape):
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    for frac in (0.02, 0.3, 0.9):
+        m = (rng.random(shape) < frac).astype(np.uint8)
+        if m.all() or not m.any():
+            continue
+        lsf = b2.tsdf_from_mask(m)
+        assert np.array_equal(lsf.phi, o.tsdf(m))
+        assert np.array_equal(b2.mask_from_phi(lsf), m)
+
+
+def test_tsdf_clip_2048():
+    clip = o.iccad_like_clip(1)
+    assert np.array_equal(b2.tsdf_from_mask(clip).phi, o.tsdf(clip))
+
+
+def test_tsdf_uniform_rejected():
+    with pytest.raises(b2.DegenerateInputError):
+        b2.tsdf_from_mask(np.zeros((8, 8), dtype=np.uint8))
+
+
+def test_elementwise_ops():
+    rng = np.random.default_rng(4)
+    v = rng.standard_normal((8, 8))
+    assert b2.cfl_timestep(np.array([[2.0, -1.0]]), 0.85) == (0.425, False)
+    assert b2.cfl_timestep(np.zeros((4, 4)), 0.85) == (0.0, True)
+    g = np.array([[1.0, 2.0], [0.0, -1.0]])
+    gp = np.ones((2, 2))
+    dp = np.array([[0.5, 0.0], [0.0, 0.5]])
+    beta = ((g * (g - gp)).sum()) / (gp * gp).sum()
+    assert np.allclose(b2.cg_direction(g, gp, dp), -g + beta * dp)
+    assert np.array_equal(b2.cg_direction(g), -g)
+    assert np.array_equal(b2.cg_direction(g, np.zeros((2, 2)), dp), -g)
+    r = b2.resist_sigmoid(np.array([0.245]), 0.225, 50.0)
+    assert abs(r[0] - 0.7310585786300049) < 1e-12
+    assert b2.resist_sigmoid(np.array([0.225]), 0.225, 50.0)[0] == 0.5
+    assert np.array_equal(b2.resist_hard(np.array([0.1, 0.225, 0.3]), 0.225), [0, 1, 1])
+    assert np.array_equal(b2.velocity(v, v, b2.OptConfig(alpha=1.0, beta=7.5)), 1.0 * v + 7.5 * v)
+    lsf = b2.LevelSetField(v)
+    with pytest.raises(b2.NumericalError, match="x=3, y=2"):
+        bad = np.zeros((8, 8))
+        bad[2, 3] = np.nan
+        b2.evolve_step(lsf, bad, 0.1)
+    out = b2.evolve_step(lsf, v, 0.1)
+    assert np.array_equal(out.phi, np.clip(v + 0.1 * v, -100.0, 900.0))
+
+
+# ---------------------------------------------------------------------------
+# the loop
+
+def _hist(r):
+    return np.array([[h.l_ilt, h.l_pvb, h.l_dso, h.dt, h.max_v, h.max_step, h.max_grad_mag]
+                     for h in r.loss_history])
+
+
+@pytest.mark.parametrize("tag", ["on", "off"])
+def test_optimize_rect128_fp64_matches_reference(tag):
+    nv.set_precision("fp64")
+    g = golden("optimize")
+    kg = golden("kernels")
+    F = ks_from((kg["17_4_1_f_c"], kg["17_4_1_f_w"]), "focus")
+    D = ks_from((kg["17_4_1_d_c"], kg["17_4_1_d_w"]), "defocus")
+    t = o.rect_layout(128, [(25, 30, 30, 50), (70, 60, 40, 40)])
+    r = b2.optimize(t, F, D, b2.OptConfig(max_iters=15, use_curvature=(tag == "on")))
+    ref = g[f"rect128_{tag}_hist"]
+    h = _hist(r)
+    assert h.shape == ref.shape
+    assert np.allclose(h, ref, rtol=1e-7, atol=1e-10)
+    assert np.array_equal(r.final_mask, g[f"rect128_{tag}_mask"])
+    l2, pvb, shots, iters = g[f"rect128_{tag}_metrics"]
+    assert (r.metrics.l2, r.metrics.pvband, r.metrics.shots, r.iters_run) == (l2, pvb, shots, iters)
+    assert np.abs(r.final_phi.phi - g[f"rect128_{tag}_phi"]).max() <= 1e-6
+
+
+@pytest.mark.parametrize("prec_name", ["fp64", "fp32"])
+@pytest.mark.parametrize("tag", ["on", "off"])
+def test_optimize_bar512_ac5(prec_name, tag):
+    """AC-5 case (512^2 two bars, K=35, N_k=8): final mask vs the reference's.
+    FP64: bit-identical mask and metrics.  FP32: pixel-flip budget 0.1% of the
+    target area and equal metrics within 2 pixels."""
+    nv.set_precision(prec_name)
+    g = golden("optimize")
+    kg = golden("kernels")
+    F = ks_from((kg["35_8_4_f_c"], kg["35_8_4_f_w"]), "focus")
+    D = ks_from((kg["35_8_4_d_c"], kg["35_8_4_d_w"]), "defocus")
+    t = o.two_bar_512()
+    r = b2.optimize(t, F, D, b2.OptConfig(max_iters=50, use_curvature=(tag == "on")))
+    ref_mask = np.unpackbits(g[f"bar512_{tag}_mask_packed"])[:512 * 512].reshape(512, 512)
+    l2, pvb, shots, iters = g[f"bar512_{tag}_metrics"]
+    flips = int((r.final_mask != ref_mask).sum())
+    if prec_name == "fp64":
+        assert flips == 0
+        assert (r.metrics.l2, r.metrics.pvband, r.metrics.shots, r.iters_run) == (l2, pvb, shots, iters)
+        assert np.allclose(_hist(r), g[f"bar512_{tag}_hist"], rtol=1e-6, atol=1e-9)
+    else:
+        assert flips <= 0.001 * t.sum()
+        assert abs(r.metrics.l2 - l2) <= 2 and abs(r.metrics.pvband - pvb) <= 2
+
+
+def test_optimize_determinism(prec):
+    f, d, F, D = kernels(17, 4, 1)
+    t = o.rect_layout(128, [(25, 30, 30, 50), (70, 60, 40, 40)])
+    r1 = b2.optimize(t, F, D, b2.OptConfig(max_iters=8))
+    r2 = b2.optimize(t, F, D, b2.OptConfig(max_iters=8))
+    assert np.array_equal(_hist(r1), _hist(r2))
+    assert np.array_equal(r1.final_phi.phi, r2.final_phi.phi)
+
+
+def test_optimize_edge_cases():
+    f, d, F, D = kernels(9, 2, 0)
+    t = o.rect_layout(128, [(25, 30, 30, 50), (70, 60, 40, 40)])
+    r = b2.optimize(t, F, D, b2.OptConfig(max_iters=0))
+    assert r.iters_run == 0 and np.array_equal(r.final_mask, t)
+    with pytest.raises(b2.DegenerateInputError):
+        b2.optimize(np.zeros((32, 32), dtype=np.uint8), F, D, b2.OptConfig())
+    with pytest.raises(ValueError):
+        b2.optimize(t, F, D, b2.OptConfig(max_iters=2), modulation=np.full(t.shape, 2.0))
+    phi0 = b2.tsdf_from_mask(t)
+    r1 = b2.optimize(t, F, D, b2.OptConfig(max_iters=5))
+    r2 = b2.optimize(t, F, D, b2.OptConfig(max_iters=5), phi0=phi0)
+    assert np.array_equal(r1.final_phi.phi, r2.final_phi.phi)
+
+
+def test_optimize_vs_oracle_fp32_rect():
+    """FP32 tier against the numpy oracle: same iteration count, loss history
+    within 1e-4 relative."""
+    nv.set_precision("fp32")
+    f, d, F, D = kernels(17, 4, 1)
+    t = o.rect_layout(128, [(25, 30, 30, 50), (70, 60, 40, 40)])
+    r = b2.optimize(t, F, D, b2.OptConfig(max_iters=12))
+    ref = o.optimize(t, f, d, o.Cfg(max_iters=12))
+    h, hr = _hist(r), np.array(ref.history)
+    assert h.shape == hr.shape
+    assert np.allclose(h[:, :3], hr[:, :3], rtol=1e-4)
+
+
+def test_clip2048_iteration0_fp32():
+    """Full-size parity (2048^2, N_k = 24): losses, prints and velocity samples
+    against the reference's own output at the initial mask."""
+    nv.set_precision("fp32")
+    g = golden("clip2048")
+    f, d, F, D = kernels(35, 24, 4)
+    clip = o.iccad_like_clip(0)
+    mask = clip.astype(np.float64)
+    cfg = b2.OptConfig()
+    p = b2.print_corners(mask, F, D, cfg, binarize=False)
+    ys, xs = g["ys"], g["xs"]
+    assert np.abs(p.nominal[ys, xs] - g["z_nom"]).max() <= 1e-5
+    assert np.abs(p.inner[ys, xs] - g["z_in"]).max() <= 1e-5
+    l_ilt = b2.ilt_loss(p.nominal, clip)
+    l_pvb = b2.pvb_loss(p.inner, p.outer, clip)
+    assert abs(l_ilt - g["l_ilt"]) <= 1e-5 * g["l_ilt"]
+    assert abs(l_pvb - g["l_pvb"]) <= 1e-5 * g["l_pvb"]
+    gi = b2.ilt_gradient(mask, p.nominal, clip, F, cfg)
+    gp = b2.pvb_gradient(mask, p.inner, p.outer, clip, F, D, cfg)
+    v = b2.velocity(gi, gp, cfg)
+    assert np.abs(v[ys, xs] - g["v"]).max() <= 1e-4 * g["v_absmax"]
+    hard = b2.print_corners(mask, F, D, cfg, binarize=True)
+    assert abs(b2.l2_error(hard.nominal, clip) - int(g["hard_l2"])) <= 4
+    assert abs(b2.pvband(hard.inner, hard.outer) - int(g["hard_pvb"])) <= 4
+
+
+def test_modulation_search_small():
+    nv.set_precision("fp64")
+    f, d, F, D = kernels(9, 2, 2)
+    target = np.zeros((64, 64), dtype=np.uint8)
+    target[16:40, 20:44] = 1
+    cfg = b2.OptConfig()
+    phi_gt = b2.tsdf_from_mask(target)
+    r = b2.modulation_search(phi_gt, target, F, D, cfg, num_samples=1, eval_steps=3)
+    assert r.best_delta_h == 0.0
+    assert np.array_equal(r.m_gt, b2.heaviside(phi_gt.phi).astype(np.float64))
+    r = b2.modulation_search(phi_gt, target, F, D, b2.OptConfig(curvature_weight=0.0),
+                             num_samples=41, eval_steps=2)
+    losses = [l for _, l in r.candidates]
+    assert max(losses) - min(losses) <= 1e-9 * max(losses)
+    assert r.best_delta_h == 0.0

@@ -1,0 +1,139 @@
+"""CPU checks of the boundary: the shared library loads without a GPU, exports
+every entry point include/lsopc_b200.h declares, and its host-only parts
+(fracturing, validation) behave like the reference."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+
+HEADER = ROOT / "include" / "lsopc_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(lsopc_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    for must in ("lsopc_plan_create", "lsopc_kset_create", "lsopc_aerial_intensity",
+                 "lsopc_print_corners", "lsopc_socs_gradient", "lsopc_tsdf",
+                 "lsopc_optimize", "lsopc_session_create", "lsopc_fracture"):
+        assert must in syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2303_12529_b200 import _native as nv
+    lib = nv.lib()
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert lib.lsopc_abi_version() == 1
+
+
+def test_fracture_native_matches_reference_counts():
+    from paper_2303_12529_b200 import metrics
+    g = golden("optimize")
+    for tag in ("on", "off"):
+        mask = g[f"rect128_{tag}_mask"]
+        assert metrics.shot_count(mask) == int(g[f"rect128_{tag}_metrics"][2])
+        bar = np.unpackbits(g[f"bar512_{tag}_mask_packed"])[:512 * 512].reshape(512, 512)
+        assert metrics.shot_count(bar) == int(g[f"bar512_{tag}_metrics"][2])
+
+
+def test_fracture_reconstructs_and_breaks_ties(rng):
+    from paper_2303_12529_b200 import metrics
+    for _ in range(10):
+        m = (rng.random((24, 31)) < 0.5).astype(np.uint8)
+        rects = metrics.fracture(m)
+        rec = np.zeros_like(m)
+        for x, y, w, h in rects:
+            assert not rec[y:y + h, x:x + w].any()
+            rec[y:y + h, x:x + w] = 1
+        assert np.array_equal(rec, m)
+    m = np.zeros((6, 6), dtype=np.uint8)
+    m[0:2, 0:2] = 1
+    m[3:5, 3:5] = 1
+    assert metrics.fracture(m)[0] == (0, 0, 2, 2)
+    plus = np.zeros((5, 5), dtype=np.uint8)
+    plus[2, :] = 1
+    plus[:, 2] = 1
+    assert metrics.shot_count(plus) == 3
+    assert metrics.fracture(np.zeros((4, 4), dtype=np.uint8)) == []
+
+
+def test_host_validation_mirrors_reference():
+    import paper_2303_12529_b200 as b2
+    with pytest.raises(ValueError):
+        b2.OptConfig(alpha=0.0, beta=0.0)
+    with pytest.raises(ValueError):
+        b2.OptConfig(eta=0.0)
+    with pytest.raises(ValueError):
+        b2.OptConfig(sigma_z=-1.0)
+    with pytest.raises(ValueError):
+        b2.OpticalKernel(np.zeros((3, 4), dtype=np.complex128), 1.0)
+    with pytest.raises(ValueError):
+        b2.OpticalKernel(np.zeros((3, 3), dtype=np.complex128), -0.1)
+    k3 = b2.OpticalKernel(np.zeros((3, 3), dtype=np.complex128), 1.0)
+    k5 = b2.OpticalKernel(np.zeros((5, 5), dtype=np.complex128), 1.0)
+    with pytest.raises(ValueError):
+        b2.KernelSet([k3, k5], "focus")
+    with pytest.raises(ValueError):
+        b2.KernelSet([k3], "blurry")
+    with pytest.raises(ValueError):
+        b2.LevelSetField(np.zeros((4, 4)), d_upper=-1.0, d_lower=-2.0)
+    cfg = b2.OptConfig()
+    assert (cfg.alpha, cfg.beta, cfg.curvature_weight, cfg.sigma_z, cfg.i_th, cfg.eta) == \
+        (1.0, 7.5, 0.9, 50.0, 0.225, 0.85)
+
+
+def test_synthetic_kernels_match_reference_bitwise():
+    import paper_2303_12529_b200 as b2
+    g = golden("kernels")
+    for side, n_k, seed in [(9, 2, 0), (17, 4, 1), (35, 8, 4)]:
+        f, d = b2.gen_synthetic_kernels(side, n_k, seed)
+        for tag, ks in (("f", f), ("d", d)):
+            assert np.array_equal(np.stack([k.coeffs for k in ks.kernels]), g[f"{side}_{n_k}_{seed}_{tag}_c"])
+            assert np.array_equal(ks.weights(), g[f"{side}_{n_k}_{seed}_{tag}_w"])
+
+
+def test_kernel_file_round_trip(tmp_path):
+    import paper_2303_12529_b200 as b2
+    f, d = b2.gen_synthetic_kernels(9, 2, seed=4)
+    p = tmp_path / "k.dvlk"
+    b2.save_kernels(p, f, d)
+    f2, d2 = b2.load_kernels(p)
+    for a, b in zip(f.kernels + d.kernels, f2.kernels + d2.kernels):
+        assert a.weight == b.weight and np.array_equal(a.coeffs, b.coeffs)
+    data = p.read_bytes()
+    p.write_bytes(data[: len(data) // 2])
+    with pytest.raises(b2.FormatError, match="byte"):
+        b2.load_kernels(p)
+    p.write_bytes(data + b"\x00")
+    with pytest.raises(b2.FormatError, match="trailing"):
+        b2.load_kernels(p)
+
+
+def test_shift_and_boundaries_host_helpers():
+    import paper_2303_12529_b200 as b2
+    g = np.array([[1.0, 2.0], [3.0, 4.0]])
+    assert np.array_equal(b2.shift(g, 1, 0, pad="replicate"), [[1, 1], [3, 3]])
+    assert np.array_equal(b2.shift(g, 0, -1), [[3, 4], [0, 0]])
+    with pytest.raises(ValueError):
+        b2.shift(g, 2, 0)
+    m = np.zeros((16, 16), dtype=np.uint8)
+    m[5, 5] = 1
+    bh, bv = b2.extract_boundaries(m)
+    eh = np.zeros((16, 16), dtype=np.uint8)
+    eh[4:7, 5] = 1
+    assert np.array_equal(bh, eh)
+
+
+def test_inputs_generators():
+    from paper_2303_12529_b200 import inputs
+    assert [int(inputs.iccad_like_clip(s).sum()) for s in (0, 1, 2)] == [333562, 308514, 334395]
+    assert inputs.two_bar_layout().sum() == 2 * 70 * 270
