@@ -173,6 +173,12 @@ int lsopc_session_phi(lsopc_session* s, double* phi_dev);
 /* Number of kernel launches one DSO iteration enqueues (bench accounting). */
 int lsopc_session_launches_per_iter(const lsopc_session* s);
 
+/* Measurement hook: enqueue `reps` launches of one spectral pass of the DSO
+ * iteration on the plan's work buffers (which: 0 forward COLS, 1 forward
+ * ROWS, 2 adjoint ROWS, 3 adjoint COLS), kernel 0 of `ks`.  Used by bench.py
+ * to time the dominant kernel with CUDA events on `stream`. */
+int lsopc_bench_pass(lsopc_plan* plan, const lsopc_kset* ks, int which, int reps, void* stream);
+
 /* fracture / shot_count (metrics.py:55-108): greedy largest all-ones
  * rectangle (ties topmost, then leftmost), host code.  rects_host may be NULL;
  * returns the count via *count. */

@@ -24,7 +24,11 @@
 
 namespace fft {
 
-constexpr int P = 16;  // complex values per thread
+// complex values held per thread: 16 for complex64 (radix <= 16), 8 for
+// complex128 (radix <= 8), keeping the register file at <= 64 regs/thread so
+// two 512-thread CTAs fit per SM.
+template <typename C> constexpr int P_of() { return sizeof(C) == 8 ? 16 : 8; }
+template <typename C> constexpr int LGP_of() { return sizeof(C) == 8 ? 4 : 3; }
 
 // ---- radix-R DFTs in registers, forward sign (exp(-2 pi i rk/R)), natural order out
 
@@ -125,16 +129,18 @@ struct Geo {
   int tws;    // log2(table length / n)
 };
 
-// Stage radices: ceil(lgn/4) stages, bits spread as evenly as possible.
-LS_D int stage_bits(int lgn, int s) {
-  int nst = (lgn + 3) >> 2;
+// Stage radices: ceil(lgn/lgp) stages, bits spread as evenly as possible.
+LS_HD int num_stages(int lgn, int lgp) { return (lgn + lgp - 1) / lgp; }
+LS_D int stage_bits(int lgn, int lgp, int s) {
+  int nst = num_stages(lgn, lgp);
   int base = lgn / nst, extra = lgn - base * nst;
   return base + (s < extra ? 1 : 0);
 }
 
 template <int RAD, bool FIRST, bool LAST, bool SEQ_FAST, bool INV, typename C, class F>
-LS_D void stage(C (&v)[P], const Geo& g, int lgNs, C* sm, const C* __restrict__ tw, F& f) {
+LS_D void stage(C (&v)[P_of<C>()], const Geo& g, int lgNs, C* sm, const C* __restrict__ tw, F& f) {
   constexpr int LGR = RAD == 2 ? 1 : RAD == 4 ? 2 : RAD == 8 ? 3 : 4;
+  constexpr int P = P_of<C>();
   const int n = 1 << g.lgn;
   const int nr = n >> LGR;  // butterflies per sequence
   const int nt = blockDim.x;
@@ -190,12 +196,14 @@ LS_D void stage(C (&v)[P], const Geo& g, int lgNs, C* sm, const C* __restrict__ 
 }
 
 template <bool FIRST, bool LAST, bool SEQ_FAST, bool INV, typename C, class F>
-LS_D void stage_rt(int bits, C (&v)[P], const Geo& g, int lgNs, C* sm, const C* tw, F& f) {
+LS_D void stage_rt(int bits, C (&v)[P_of<C>()], const Geo& g, int lgNs, C* sm, const C* tw, F& f) {
   switch (bits) {
     case 1: stage<2, FIRST, LAST, SEQ_FAST, INV>(v, g, lgNs, sm, tw, f); break;
     case 2: stage<4, FIRST, LAST, SEQ_FAST, INV>(v, g, lgNs, sm, tw, f); break;
     case 3: stage<8, FIRST, LAST, SEQ_FAST, INV>(v, g, lgNs, sm, tw, f); break;
-    default: stage<16, FIRST, LAST, SEQ_FAST, INV>(v, g, lgNs, sm, tw, f); break;
+    default:
+      if constexpr (P_of<C>() >= 16) stage<16, FIRST, LAST, SEQ_FAST, INV>(v, g, lgNs, sm, tw, f);
+      break;
   }
 }
 
@@ -203,22 +211,23 @@ LS_D void stage_rt(int bits, C (&v)[P], const Geo& g, int lgNs, C* sm, const C* 
 // (the launcher guarantees it).  The first stage peels the twiddle (Ns=1).
 template <bool SEQ_FAST, bool INV, typename C, class F>
 LS_D void run(const Geo& g, C* sm, const C* __restrict__ tw, F& f) {
-  C v[P];
-  const int nst = (g.lgn + 3) >> 2;
+  constexpr int LGP = LGP_of<C>();
+  C v[P_of<C>()];
+  const int nst = num_stages(g.lgn, LGP);
   if (nst == 1) {
-    stage_rt<true, true, SEQ_FAST, INV>(stage_bits(g.lgn, 0), v, g, 0, sm, tw, f);
+    stage_rt<true, true, SEQ_FAST, INV>(stage_bits(g.lgn, LGP, 0), v, g, 0, sm, tw, f);
     return;
   }
   int lgNs = 0;
-  int b0 = stage_bits(g.lgn, 0);
+  int b0 = stage_bits(g.lgn, LGP, 0);
   stage_rt<true, false, SEQ_FAST, INV>(b0, v, g, 0, sm, tw, f);
   lgNs += b0;
   for (int s = 1; s < nst - 1; ++s) {
-    int bs = stage_bits(g.lgn, s);
+    int bs = stage_bits(g.lgn, LGP, s);
     stage_rt<false, false, SEQ_FAST, INV>(bs, v, g, lgNs, sm, tw, f);
     lgNs += bs;
   }
-  stage_rt<false, true, SEQ_FAST, INV>(stage_bits(g.lgn, nst - 1), v, g, lgNs, sm, tw, f);
+  stage_rt<false, true, SEQ_FAST, INV>(stage_bits(g.lgn, LGP, nst - 1), v, g, lgNs, sm, tw, f);
 }
 
 }  // namespace fft

@@ -1,0 +1,98 @@
+// Greedy rectangle fracturing / shot count (host code), replacing
+// fracture + _largest_rect (metrics.py:55-108).
+//
+// Reference semantics: repeatedly take the largest-area all-ones rectangle,
+// ties broken topmost then leftmost (the first candidate met by a row-major
+// histogram-stack sweep), and clear it.  The reference re-sweeps the whole
+// mask every round (O(shots * H * W)).  Here the sweep result is cached per
+// bottom row: clearing a rectangle only changes the column heights of its
+// columns from its top row down to where each column run ends, so only those
+// rows are re-swept.  Scanning the cached row bests in row order with the
+// reference's strict comparison returns exactly the reference's pick.
+#include "../../include/lsopc_b200.h"
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace {
+
+struct Cand {
+  long long area = 0;
+  int x = 0, y = 0, w = 0, h = 0;
+};
+
+// metrics.py:80-84 ordering: larger area, then smaller top, then smaller left
+inline bool better(const Cand& c, const Cand& best) {
+  return c.area > best.area || (c.area == best.area && (c.y < best.y || (c.y == best.y && c.x < best.x)));
+}
+
+// histogram-stack sweep of one bottom row (metrics.py:67-86)
+Cand sweep_row(const int* heights, int W, int y, std::vector<int>& stack) {
+  Cand best;
+  int top = -1;
+  for (int x = 0; x <= W; ++x) {
+    const int cur = x < W ? heights[x] : 0;
+    while (top >= 0 && heights[stack[top]] > cur) {
+      const int hh = heights[stack[top]];
+      --top;
+      const int left = top >= 0 ? stack[top] + 1 : 0;
+      Cand c;
+      c.area = (long long)hh * (x - left);
+      c.x = left;
+      c.y = y - hh + 1;
+      c.w = x - left;
+      c.h = hh;
+      if (better(c, best)) best = c;
+    }
+    stack[++top] = x;
+  }
+  return best;
+}
+
+}  // namespace
+
+extern "C" int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* rects, size_t cap,
+                              size_t* count) {
+  if (H < 0 || W < 0 || !count) return LSOPC_EINVAL;
+  std::vector<uint8_t> m((size_t)H * W);
+  for (size_t i = 0; i < m.size(); ++i) m[i] = mask_host[i] != 0;
+  std::vector<int> hts((size_t)H * W, 0);
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      size_t p = (size_t)y * W + x;
+      hts[p] = m[p] ? (y > 0 ? hts[p - W] : 0) + 1 : 0;
+    }
+  std::vector<int> stack(W + 1);
+  std::vector<Cand> rowbest(H);
+  for (int y = 0; y < H; ++y) rowbest[y] = sweep_row(&hts[(size_t)y * W], W, y, stack);
+  size_t k = 0;
+  while (true) {
+    Cand best;
+    for (int y = 0; y < H; ++y)
+      if (better(rowbest[y], best)) best = rowbest[y];
+    if (best.area == 0) break;
+    if (rects && k < cap) {
+      rects[4 * k] = best.x;
+      rects[4 * k + 1] = best.y;
+      rects[4 * k + 2] = best.w;
+      rects[4 * k + 3] = best.h;
+    }
+    ++k;
+    for (int yy = best.y; yy < best.y + best.h; ++yy) std::memset(&m[(size_t)yy * W + best.x], 0, best.w);
+    // refresh the heights of the cleared columns from the rectangle's top row down
+    int ymax = best.y + best.h - 1;
+    for (int x = best.x; x < best.x + best.w; ++x) {
+      for (int y = best.y; y < H; ++y) {
+        size_t p = (size_t)y * W + x;
+        int nh = m[p] ? (y > 0 ? hts[p - W] : 0) + 1 : 0;
+        if (y >= best.y + best.h && nh == hts[p]) break;
+        hts[p] = nh;
+        if (y > ymax) ymax = y;
+      }
+    }
+    for (int y = best.y; y <= ymax; ++y) rowbest[y] = sweep_row(&hts[(size_t)y * W], W, y, stack);
+  }
+  *count = k;
+  return LSOPC_OK;
+}

@@ -74,4 +74,9 @@ void launch_gate(const Grid& g, const double* z, const double* zt, double scale,
 // copy the first field of A (element C) to complex128
 void launch_to_c128(const Grid& g, const void* A, double* out, cudaStream_t s);
 
+// one launch of a single spectral pass for measurement:
+// 0 forward COLS, 1 forward ROWS, 2 adjoint ROWS, 3 adjoint COLS
+void launch_bench_pass(const Grid& g, int which, const void* spec, void* mhat, void* A, void* I, void* gate,
+                       void* G, void* scratch, cudaStream_t s);
+
 }  // namespace lsb

@@ -150,7 +150,7 @@ template <typename R> struct FFinish : Pos<true> {
 };
 
 template <typename R, bool SEQ_FAST, bool INV, class F>
-__global__ void __launch_bounds__(512) k_fft(F f, fft::Geo geo, const typename CT<R>::C* __restrict__ tw,
+__global__ void __launch_bounds__(512, 2) k_fft(F f, fft::Geo geo, const typename CT<R>::C* __restrict__ tw,
                                              StopFlag stop) {
   using C = typename CT<R>::C;
   if (stop && *stop) return;
@@ -177,7 +177,7 @@ int launch_pass(const Grid& g, F f, const void* tw, StopFlag stop, cudaStream_t 
   const int n = 1 << lgn;
   const int E = std::max(elems_per_cta<R>(), n);
   const int nb = std::min(E / n, nseq);
-  const int threads = nb * n / fft::P;
+  const int threads = nb * n / fft::P_of<C>();
   if (threads < 1) throw std::runtime_error("grid too small for the FFT engine (need H*W >= 16)");
   fft::Geo geo{lgn, nb, ilog2(nb), g.lgnmax - lgn};
   const size_t smem = std::max(fft::smem_bytes<C>(n, nb), (size_t)(64 * sizeof(double)));
@@ -185,6 +185,7 @@ int launch_pass(const Grid& g, F f, const void* tw, StopFlag stop, cudaStream_t 
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr_set = true;
   }
   f.W = g.W;
@@ -371,6 +372,55 @@ void launch_to_c128(const Grid& g, const void* A, double* out, cudaStream_t s) {
 }
 
 int reduce_blocks() { return kRedBlocks; }
+
+namespace {
+template <typename R>
+void bench_pass_impl(const Grid& g, int which, const void* spec, void* mhat, void* A, void* I, void* gate,
+                     void* G, void* scratch, cudaStream_t s) {
+  using C = typename CT<R>::C;
+  switch (which) {
+    case 0: {
+      FFwdCol<R> f;
+      f.mhat = static_cast<const C*>(mhat);
+      f.spec = static_cast<const C*>(spec);
+      f.scale = (R)1;
+      f.y = static_cast<C*>(scratch);
+      launch_pass<R, false, true>(g, f, g.tw, nullptr, s);
+    } break;
+    case 1: {
+      FFwdRow<R> f;
+      f.x = static_cast<const C*>(scratch);
+      f.a = static_cast<C*>(A);
+      f.I = static_cast<R*>(I);
+      f.w = (R)1;
+      f.first = 0;
+      launch_pass<R, true, true>(g, f, g.tw, nullptr, s);
+    } break;
+    case 2: {
+      FAdjRow<R> f;
+      f.a = static_cast<const C*>(A);
+      f.gate = static_cast<const R*>(gate);
+      f.y = static_cast<C*>(scratch);
+      launch_pass<R, true, false>(g, f, g.tw, nullptr, s);
+    } break;
+    default: {
+      FAdjCol<R> f;
+      f.x = static_cast<const C*>(scratch);
+      f.spec = static_cast<const C*>(spec);
+      f.w = (R)1;
+      f.G = static_cast<C*>(G);
+      f.first = 0;
+      launch_pass<R, false, false>(g, f, g.tw, nullptr, s);
+    } break;
+  }
+}
+}  // namespace
+
+void launch_bench_pass(const Grid& g, int which, const void* spec, void* mhat, void* A, void* I, void* gate,
+                       void* G, void* scratch, cudaStream_t s) {
+  if (g.prec == F64) bench_pass_impl<double>(g, which, spec, mhat, A, I, gate, G, scratch, s);
+  else bench_pass_impl<float>(g, which, spec, mhat, A, I, gate, G, scratch, s);
+}
 
 void launch_kernel_spectra(const Grid& g, int nk, int K, const double* coeffs_dev, void* spec,
                            void* scratch, cudaStream_t s) {

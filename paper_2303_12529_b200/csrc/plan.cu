@@ -607,6 +607,20 @@ int lsopc_session_destroy(lsopc_session* ss) {
   });
 }
 
+int lsopc_bench_pass(lsopc_plan* plan, const lsopc_kset* ks, int which, int reps, void* stream) {
+  return guarded([&] {
+    check_plan(plan);
+    check_kset(plan, ks);
+    if (which < 0 || which > 3) throw Error(LSOPC_EINVAL, "bad pass id");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    plan->A.ensure(plan->n() * plan->g.csize());
+    for (int r = 0; r < reps; ++r)
+      launch_bench_pass(plan->g, which, ks->spec.p, plan->mhat.p, plan->A.p, plan->If.p, plan->wf.p, plan->G.p,
+                        plan->scratch.p, s);
+    ck_launch("bench pass");
+  });
+}
+
 int lsopc_session_launches_per_iter(const lsopc_session* ss) {
   if (!ss) return 0;
   // mask fft 2, forward 2 per kernel, resist+after 2, copy 1, adjoint 2 per kernel,
@@ -637,61 +651,5 @@ int lsopc_optimize(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_kset* 
   return rc;
 }
 
-// metrics.py:55-87 _largest_rect: histogram stack sweep, ties topmost then leftmost
-static void largest_rect(const std::vector<uint8_t>& m, int H, int W, std::vector<long long>& heights,
-                         std::vector<int>& stack, long long& best, int& bx, int& by, int& bw, int& bh) {
-  std::fill(heights.begin(), heights.end(), 0);
-  best = 0;
-  bx = by = bw = bh = 0;
-  for (int y = 0; y < H; ++y) {
-    const uint8_t* row = &m[(size_t)y * W];
-    for (int x = 0; x < W; ++x) heights[x] = row[x] ? heights[x] + 1 : 0;
-    int top = -1;
-    for (int x = 0; x <= W; ++x) {
-      long long cur = x < W ? heights[x] : 0;
-      while (top >= 0 && heights[stack[top]] > cur) {
-        long long hh = heights[stack[top]];
-        --top;
-        int left = top >= 0 ? stack[top] + 1 : 0;
-        int width = x - left;
-        long long area = hh * width;
-        int ty = y - (int)hh + 1;
-        if (area > best || (area == best && (ty < by || (ty == by && left < bx)))) {
-          best = area;
-          bx = left;
-          by = ty;
-          bw = width;
-          bh = (int)hh;
-        }
-      }
-      stack[++top] = x;
-    }
-  }
-}
-
-int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* rects, size_t cap, size_t* count) {
-  return guarded([&] {
-    std::vector<uint8_t> work((size_t)H * W);
-    for (size_t i = 0; i < work.size(); ++i) work[i] = mask_host[i] != 0;
-    std::vector<long long> heights(W);
-    std::vector<int> stack(W + 1);
-    size_t k = 0;
-    while (true) {
-      long long area;
-      int x, y, w, h;
-      largest_rect(work, H, W, heights, stack, area, x, y, w, h);
-      if (area == 0) break;
-      if (rects && k < cap) {
-        rects[4 * k] = x;
-        rects[4 * k + 1] = y;
-        rects[4 * k + 2] = w;
-        rects[4 * k + 3] = h;
-      }
-      ++k;
-      for (int yy = y; yy < y + h; ++yy) std::memset(&work[(size_t)yy * W + x], 0, w);
-    }
-    *count = k;
-  });
-}
 
 }  // extern "C"

@@ -127,6 +127,17 @@ def main():
                                                  r.metrics.shots, r.iters_run])
     np.savez_compressed(OUT / "optimize.npz", **opt)
 
+    # ---- fracture (metrics.fracture): rectangle lists on random masks ---------
+    from lsopc import metrics
+    fr = {}
+    rng = np.random.default_rng(77)
+    for i in range(12):
+        h, w = int(rng.integers(3, 48)), int(rng.integers(3, 48))
+        m = (rng.random((h, w)) < rng.uniform(0.2, 0.95)).astype(np.uint8)
+        fr[f"mask{i}"] = m
+        fr[f"rects{i}"] = np.array(metrics.fracture(m), dtype=np.int64).reshape(-1, 4)
+    np.savez_compressed(OUT / "fracture.npz", **fr)
+
     if big:
         # full-size samples: 2048^2 iccad-like clip 0, N_k = 24, iteration 0
         sys.path.insert(0, str(OUT.parents[1]))

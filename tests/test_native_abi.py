@@ -137,3 +137,11 @@ def test_inputs_generators():
     from paper_2303_12529_b200 import inputs
     assert [int(inputs.iccad_like_clip(s).sum()) for s in (0, 1, 2)] == [333562, 308514, 334395]
     assert inputs.two_bar_layout().sum() == 2 * 70 * 270
+
+
+def test_fracture_matches_reference_rect_lists():
+    from paper_2303_12529_b200 import metrics
+    g = golden("fracture")
+    for i in range(12):
+        got = metrics.fracture(g[f"mask{i}"])
+        assert got == [tuple(int(v) for v in r) for r in g[f"rects{i}"]]
