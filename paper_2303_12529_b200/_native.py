@@ -34,7 +34,7 @@ class LsopcConfig(ctypes.Structure):
                 ("d_upper", ctypes.c_double), ("d_lower", ctypes.c_double),
                 ("max_iters", ctypes.c_int), ("stop_rel_tol", ctypes.c_double),
                 ("stop_patience", ctypes.c_int), ("use_curvature", ctypes.c_int),
-                ("cg_restart_every", ctypes.c_int)]
+                ("cg_restart_every", ctypes.c_int), ("update_form", ctypes.c_int)]
 
 
 class LsopcResult(ctypes.Structure):
