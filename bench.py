@@ -164,17 +164,27 @@ def algorithmic_bytes_per_iter(n, n_k_total, prec):
     return n * (64 * nk + 170) if prec == "fp32" else n * (128 * nk + 230)
 
 
-def pass_bytes(which, n, prec):
+PASS_NAMES = ["mask_fft (rows+cols)", "F1 forward cols: T_k = IFFT_y(M^.H_k)",
+              "F2 forward rows: I = sum w|IFFT_x T_k|^2", "resist/loss/best",
+              "A1 adjoint rows: U_k = FFT_x(gate.IFFT_x T_k)",
+              "A2 adjoint cols: V = IFFT_y(sum w conj(H_k).FFT_y U_k)", "A3 finish: g = Re IFFT_x V (+CG dots)",
+              "level-set step (velocity, CFL, update)"]
+
+
+def pass_bytes(n, nk_tot, nsets, prec):
+    """Algorithmic HBM bytes of each pass of one DSO iteration:
+    c = complex element, r = real element of the transform tier."""
     c = 8 if prec == "fp32" else 16
     r = 4 if prec == "fp32" else 8
-    return {0: 3 * c * n,            # forward COLS: read M^, H_k; write B
-            1: (2 * c + 2 * r) * n,  # forward ROWS: read B, I; write A_k, I
-            2: (2 * c + r) * n,      # adjoint ROWS: read A_k, gate; write C
-            3: 4 * c * n}[which]     # adjoint COLS: read C, H_k, G; write G
-
-
-PASS_NAMES = {0: "forward_cols (y-IFFT of M^.H_k)", 1: "forward_rows (x-IFFT, |A|^2 accumulate)",
-              2: "adjoint_rows (x-FFT of gate.A_k)", 3: "adjoint_cols (y-FFT, conj(H_k) accumulate)"}
+    per_px = [1 + 4 * c,                       # u8 mask in, M~ out+in, M^ out
+              nk_tot * 2 * c + nsets * c,      # H_k in, T_k out; M^ tile once per (tile, set)
+              nk_tot * c + nsets * r,          # T_k in; I_set out
+              4 * r + 1,                       # I_f, I_d in; gates out; target in
+              nk_tot * 2 * c + nsets * r,      # T_k in, U_k out; gate once per (block, set)
+              nk_tot * 2 * c + nsets * c,      # U_k in, H_k in; V_set out
+              2 * c + 24,                      # V_f, V_d in; v out; v_prev in (dots)
+              73]                              # phi stencil, v, d_prev, m in; d, u out; phi, mask out
+    return [p * n for p in per_px]
 
 
 def b200_arm(args, world, rank, local):
@@ -203,7 +213,7 @@ def b200_arm(args, world, rank, local):
     L = nv.lib()
 
     # ---- device-resident timing: W warm-up + K timed iterations --------------
-    cfg = b2.OptConfig(max_iters=W + K, stop_patience=10**9, precision=args.precision)
+    cfg = b2.OptConfig(max_iters=W + K + 5, stop_patience=10**9, precision=args.precision)
     c = b2.optimizer._native_cfg(cfg)
     td = nv.to_dev(clip, np.uint8)
     sess = ctypes.c_void_p()
@@ -227,7 +237,6 @@ def b200_arm(args, world, rank, local):
     ms = ev0.elapsed_time(ev1)
     nv.check(L.lsopc_session_poll(sess, ctypes.byref(stopped), None))
     assert not stopped.value, "stop rule fired inside the timed region"
-    L.lsopc_session_destroy(sess)
     ms_max = ms
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -235,23 +244,19 @@ def b200_arm(args, world, rank, local):
         ms_max = float(t.item())
     value = world * K / (ms_max / 1e3)
 
-    # ---- dominant kernel: per-pass CUDA-event timing -------------------------
+    # ---- per-pass CUDA-event timing on the session stream (after the timed region)
     pk, src = peaks()
     hbm = float(pk["hbm_gbs"])
+    ms_pass = (ctypes.c_double * 8)()
+    nv.check(L.lsopc_session_time_passes(sess, 5, ms_pass))
+    L.lsopc_session_destroy(sess)
+    pb = pass_bytes(n, 2 * N_K, 2, args.precision)
     per_pass = {}
-    for which in range(4):
-        nv.check(L.lsopc_bench_pass(fk.plan.handle, fk.handle, which, 3, sp))
-        torch.cuda.synchronize()
-        reps = 40
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        nv.check(L.lsopc_bench_pass(fk.plan.handle, fk.handle, which, reps, sp))
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t_launch = e0.elapsed_time(e1) / reps / 1e3
-        b = pass_bytes(which, n, args.precision)
-        per_pass[which] = {"name": PASS_NAMES[which], "us": t_launch * 1e6, "bytes": b,
-                           "gbs": b / t_launch / 1e9, "frac": b / t_launch / 1e9 / hbm}
+    for i in range(8):
+        t = ms_pass[i] / 1e3
+        per_pass[i] = {"name": PASS_NAMES[i], "us": t * 1e6, "bytes": pb[i],
+                       "gbs": pb[i] / t / 1e9 if t > 0 else 0.0,
+                       "frac": pb[i] / t / 1e9 / hbm if t > 0 else 0.0}
     dom = max(per_pass, key=lambda w: per_pass[w]["us"])
     iter_s = ms / 1e3 / K
     b_iter = algorithmic_bytes_per_iter(n, 2 * N_K, args.precision)
@@ -326,8 +331,12 @@ def b200_arm(args, world, rank, local):
                                                         "GBps": round(per_pass[w]["gbs"], 1),
                                                         "frac": round(per_pass[w]["frac"], 4)}
                                   for w in per_pass},
-                     "iteration": {"algorithmic_bytes": b_iter, "achieved_GBps": round(b_iter / iter_s / 1e9, 1),
-                                   "frac": round(b_iter / iter_s / 1e9 / hbm, 4)}},
+                     "iteration": {"algorithmic_bytes_survey": b_iter,
+                                   "achieved_GBps_survey": round(b_iter / iter_s / 1e9, 1),
+                                   "frac_survey": round(b_iter / iter_s / 1e9 / hbm, 4),
+                                   "pass_bytes": sum(pb),
+                                   "achieved_GBps_passes": round(sum(pb) / iter_s / 1e9, 1),
+                                   "frac_passes": round(sum(pb) / iter_s / 1e9 / hbm, 4)}},
         "cpu_baseline": cpu,
         "gpu_launches": launches_per_iter * K,
         "clocks": clk.summary(),

@@ -173,11 +173,13 @@ int lsopc_session_phi(lsopc_session* s, double* phi_dev);
 /* Number of kernel launches one DSO iteration enqueues (bench accounting). */
 int lsopc_session_launches_per_iter(const lsopc_session* s);
 
-/* Measurement hook: enqueue `reps` launches of one spectral pass of the DSO
- * iteration on the plan's work buffers (which: 0 forward COLS, 1 forward
- * ROWS, 2 adjoint ROWS, 3 adjoint COLS), kernel 0 of `ks`.  Used by bench.py
- * to time the dominant kernel with CUDA events on `stream`. */
-int lsopc_bench_pass(lsopc_plan* plan, const lsopc_kset* ks, int which, int reps, void* stream);
+/* Measurement hook: run `reps` more iterations of the session, recording CUDA
+ * events on the session stream at the pass boundaries, and write the mean
+ * per-iteration milliseconds of each pass to ms_out[8]:
+ * 0 mask FFT (2 launches), 1 F1 forward columns, 2 F2 forward rows + intensity,
+ * 3 resist/loss/best (3 launches), 4 A1 adjoint rows, 5 A2 adjoint columns,
+ * 6 A3 adjoint finish + CG dots, 7 level-set step (5 launches).  Synchronises. */
+int lsopc_session_time_passes(lsopc_session* s, int reps, double* ms_out);
 
 /* fracture / shot_count (metrics.py:55-108): greedy largest all-ones
  * rectangle (ties topmost, then leftmost), host code.  rects_host may be NULL;

@@ -75,7 +75,7 @@ _SIGS = {
     "lsopc_session_destroy": (_I, [_P]),
     "lsopc_session_launches_per_iter": (_I, [_P]),
     "lsopc_fracture": (_I, [_I, _I, _P, _P, _Z, ctypes.POINTER(_Z)]),
-    "lsopc_bench_pass": (_I, [_P, _P, _I, _I, _P]),
+    "lsopc_session_time_passes": (_I, [_P, _I, ctypes.POINTER(_D)]),
 }
 
 _lib = None

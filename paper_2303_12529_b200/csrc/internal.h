@@ -24,33 +24,57 @@ struct Grid {
 // (the device-side stop rule of the optimisation loop).
 using StopFlag = const int*;
 
-// spectrum of one kernel set: nk x [H][W] complex (element C of the grid)
-// coeffs_dev: nk x K x K interleaved complex128; scratch: >= H*W*16 bytes
-void launch_kernel_spectra(const Grid& g, int nk, int K, const double* coeffs_dev,
-                           void* spec, void* scratch, cudaStream_t s);
+inline int ilog2i(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
 
-// M^ = FFT2(mask) ; mask is u8 (mask_u8 != null) or f64
-void launch_mask_fft(const Grid& g, const uint8_t* mask_u8, const double* mask_f64,
+// One SOCS kernel set as seen by the spectral passes (spectral.cu).  All
+// complex fields are column-tiled (engine.cuh) in the plan's precision.
+struct SpecSet {
+  int nk;
+  const double* w;   // host weights (sigma_k), nk
+  const void* spec;  // nk spectra
+  void* T;           // nk work fields: T_k after the forward, U_k after A1
+  void* I;           // real intensity sum_k w_k |A_k|^2, row-major (element R)
+  const void* gate;  // real gate, row-major (element R)
+  void* V;           // complex adjoint accumulator (column-tiled)
+};
+
+// K0: spectra of nk K x K kernels (float64 transform, stored in plan precision)
+// coeffs_dev: nk x K x K interleaved complex128; scratch, scratch2: >= H*W*16 bytes
+void launch_kernel_spectra(const Grid& g, int nk, int K, const double* coeffs_dev, void* spec,
+                           void* scratch, void* scratch2, cudaStream_t s);
+// one spectrum (plan precision, column-tiled) -> complex128 row-major
+void launch_spec_to_c128(const Grid& g, const void* field, double* out, cudaStream_t s);
+
+// M^ = FFT2(mask); exactly one of mask_u8 / mask_f64 / phi (mask = phi <= 0) is non-null.
+// scratch >= H*W complex elements.
+void launch_mask_fft(const Grid& g, const uint8_t* mask_u8, const double* mask_f64, const double* phi,
                      void* mhat, void* scratch, StopFlag stop, cudaStream_t s);
 
-// forward for one kernel set: for each k, A_k = IFFT2(M^ H_k); I = sum_k w_k |A_k|^2
-// A (nullable) receives nk fields; I is element R.
-void launch_forward_set(const Grid& g, int nk, const void* mhat, const void* spec,
-                        const double* weights_host, void* A, void* I, void* scratch,
-                        StopFlag stop, cudaStream_t s);
+// forward of nsets (1 or 2) sets: T_k = IFFT_y(M^ H_k)/(HW), I = sum_k w_k |IFFT_x T_k|^2.
+// a0_c128 (nullable): the first set's first field A_0 as complex128 row-major.
+void launch_forward(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, double* a0_c128,
+                    StopFlag stop, cudaStream_t s);
 
-// adjoint for one kernel set, accumulated into G (first==true overwrites):
-// G += sum_k w_k conj(H_k) FFT2(gate * A_k)
-void launch_adjoint_set(const Grid& g, int nk, const void* A, const void* gate,
-                        const void* spec, const double* weights_host, void* G, bool first,
-                        void* scratch, StopFlag stop, cudaStream_t s);
+// the two halves of launch_forward / launch_adjoint (per-pass timing)
+void launch_f1(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
+void launch_f2(const Grid& g, const SpecSet* sets, int nsets, double* a0_c128, StopFlag stop, cudaStream_t s);
+void launch_a1(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
+void launch_a2(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
 
-// out = scale * Re IFFT2_unnormalised(G)  (f64 out); optional CG dot partials
-// with v_prev: dots[blk*2 + {0,1}] = {sum v (v - vp), sum vp^2} over the block.
-// Returns the number of dot partial blocks written (0 when v_prev is null).
-int launch_adjoint_finish(const Grid& g, const void* G, double scale, double* out,
-                          const double* v_prev, double* dots, void* scratch,
-                          StopFlag stop, cudaStream_t s);
+// adjoint of nsets sets: U_k = FFT_x(gate IFFT_x T_k) (in place),
+// V = IFFT_y(sum_k w_k conj(H_k) FFT_y U_k)
+void launch_adjoint(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
+
+// out = scale * Re IFFT_x(V0 [+ V1]) (f64 row-major); with v_prev, per-CTA CG dot
+// partials dots[blk*2 + {0,1}] = {sum v (v - vp), sum vp^2}.  Returns the
+// number of partial blocks written (0 without v_prev).
+int launch_adjoint_finish(const Grid& g, const void* V0, const void* V1, double scale, double* out,
+                          const double* v_prev, double* dots, StopFlag stop, cudaStream_t s);
+int finish_max_blocks();
 
 // ---- elementwise / reductions ---------------------------------------------------
 int reduce_blocks();   // number of partial slots used by grid-stride reducers
@@ -70,13 +94,5 @@ void launch_scale_intensity(const Grid& g, const void* I, double dose, double* o
 // gate for a user-supplied print: w = scale * (z - zt) z (1 - z)   (element R)
 void launch_gate(const Grid& g, const double* z, const double* zt, double scale, void* w,
                  cudaStream_t s);
-
-// copy the first field of A (element C) to complex128
-void launch_to_c128(const Grid& g, const void* A, double* out, cudaStream_t s);
-
-// one launch of a single spectral pass for measurement:
-// 0 forward COLS, 1 forward ROWS, 2 adjoint ROWS, 3 adjoint COLS
-void launch_bench_pass(const Grid& g, int which, const void* spec, void* mhat, void* A, void* I, void* gate,
-                       void* G, void* scratch, cudaStream_t s);
 
 }  // namespace lsb

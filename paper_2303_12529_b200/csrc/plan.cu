@@ -70,13 +70,16 @@ struct DevBuf {
 
 struct lsopc_plan {
   Grid g{};
-  DevBuf tw, tw64, mhat, scratch, G, If, Id, wf, wd, partials, scal, A, hard, tsdf_i, tsdf_f;
+  // T: per-kernel work fields (T_k / U_k) of the spectral passes, grown to the
+  // largest (focus + defocus) kernel count used on this plan.
+  DevBuf tw, tw64, mhat, scratch, scratch2, T, V0, V1, If, Id, wf, wd, partials, scal, hard, tsdf_i, tsdf_f;
   ~lsopc_plan() {
-    for (DevBuf* b : {&tw, &tw64, &mhat, &scratch, &G, &If, &Id, &wf, &wd, &partials, &scal, &A, &hard, &tsdf_i,
-                      &tsdf_f})
+    for (DevBuf* b : {&tw, &tw64, &mhat, &scratch, &scratch2, &T, &V0, &V1, &If, &Id, &wf, &wd, &partials, &scal,
+                      &hard, &tsdf_i, &tsdf_f})
       b->release();
   }
   size_t n() const { return g.n(); }
+  void ensure_T(int nk_total) { T.ensure((size_t)nk_total * n() * g.csize()); }
 };
 
 struct lsopc_kset {
@@ -118,9 +121,25 @@ double reduce_to_host(int op, size_t n, const double* a, const double* b, const 
   return h;
 }
 
-// forward of one set into If/Id with (optional) field storage at A offset
-void forward(lsopc_plan* p, const lsopc_kset* ks, void* I, void* A, StopFlag stop, cudaStream_t s) {
-  launch_forward_set(p->g, ks->nk, p->mhat.p, ks->spec.p, ks->w.data(), A, I, p->scratch.p, stop, s);
+// SpecSet views of one or two kernel sets on the plan's work buffers
+SpecSet spec_set(lsopc_plan* p, const lsopc_kset* ks, int which, size_t T_off_kernels) {
+  SpecSet s{};
+  s.nk = ks->nk;
+  s.w = ks->w.data();
+  s.spec = ks->spec.p;
+  s.T = static_cast<char*>(p->T.p) + T_off_kernels * p->n() * p->g.csize();
+  s.I = which == 0 ? p->If.p : p->Id.p;
+  s.gate = which == 0 ? p->wf.p : p->wd.p;
+  s.V = which == 0 ? p->V0.p : p->V1.p;
+  return s;
+}
+
+// forward of one set (I into If) or of focus + defocus (If, Id)
+void forward(lsopc_plan* p, const lsopc_kset* f, const lsopc_kset* d, StopFlag stop, cudaStream_t s,
+             double* a0_c128 = nullptr) {
+  p->ensure_T(f->nk + (d ? d->nk : 0));
+  SpecSet sets[2] = {spec_set(p, f, 0, 0), d ? spec_set(p, d, 1, f->nk) : SpecSet{}};
+  launch_forward(p->g, p->mhat.p, sets, d ? 2 : 1, a0_c128, stop, s);
   ck_launch("forward");
 }
 
@@ -171,7 +190,9 @@ int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
       const size_t n = p->n();
       p->mhat.ensure(n * p->g.csize());
       p->scratch.ensure(n * 16);
-      p->G.ensure(n * p->g.csize());
+      p->scratch2.ensure(n * 16);
+      p->V0.ensure(n * p->g.csize());
+      p->V1.ensure(n * p->g.csize());
       p->If.ensure(n * p->g.rsize());
       p->Id.ensure(n * p->g.rsize());
       p->wf.ensure(n * p->g.rsize());
@@ -215,7 +236,7 @@ int lsopc_kset_create(lsopc_plan* plan, int n_k, int K, const double* coeffs_hos
       const size_t cb = (size_t)n_k * K * K * 2 * sizeof(double);
       coeffs.ensure(cb);
       ck(cudaMemcpyAsync(coeffs.p, coeffs_host, cb, cudaMemcpyHostToDevice, s), "memcpy");
-      launch_kernel_spectra(plan->g, n_k, K, coeffs.as<double>(), ks->spec.p, plan->scratch.p, s);
+      launch_kernel_spectra(plan->g, n_k, K, coeffs.as<double>(), ks->spec.p, plan->scratch.p, plan->scratch2.p, s);
       ck_launch("kernel spectra");
       ck(cudaStreamSynchronize(s), "sync");
       coeffs.release();
@@ -234,7 +255,7 @@ int lsopc_kset_download(const lsopc_kset* ks, double* out, void* stream) {
     const size_t n = ks->plan->n();
     Grid g = ks->plan->g;
     for (int k = 0; k < ks->nk; ++k) {
-      launch_to_c128(g, static_cast<const char*>(ks->spec.p) + (size_t)k * n * g.csize(), out + (size_t)k * n * 2, s);
+      launch_spec_to_c128(g, static_cast<const char*>(ks->spec.p) + (size_t)k * n * g.csize(), out + (size_t)k * n * 2, s);
       ck_launch("download");
     }
   });
@@ -253,9 +274,9 @@ int lsopc_aerial_intensity(lsopc_plan* plan, const lsopc_kset* ks, const double*
     check_plan(plan);
     check_kset(plan, ks);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_mask_fft(plan->g, nullptr, mask_dev, plan->mhat.p, plan->scratch.p, nullptr, s);
+    launch_mask_fft(plan->g, nullptr, mask_dev, nullptr, plan->mhat.p, plan->scratch.p, nullptr, s);
     ck_launch("mask fft");
-    forward(plan, ks, plan->If.p, nullptr, nullptr, s);
+    forward(plan, ks, nullptr, nullptr, s);
     launch_scale_intensity(plan->g, plan->If.p, dose, out_dev, s);
     ck_launch("scale intensity");
   });
@@ -269,10 +290,9 @@ int lsopc_print_corners(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_k
     check_kset(plan, focus);
     check_kset(plan, defocus);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_mask_fft(plan->g, nullptr, mask_dev, plan->mhat.p, plan->scratch.p, nullptr, s);
+    launch_mask_fft(plan->g, nullptr, mask_dev, nullptr, plan->mhat.p, plan->scratch.p, nullptr, s);
     ck_launch("mask fft");
-    forward(plan, focus, plan->If.p, nullptr, nullptr, s);
-    forward(plan, defocus, plan->Id.p, nullptr, nullptr, s);
+    forward(plan, focus, defocus, nullptr, s);
     ResistParams rp{i_th, sigma_z, 0.0, 0.0};
     if (binarize)
       launch_resist(plan->g, plan->If.p, plan->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr,
@@ -293,17 +313,16 @@ int lsopc_socs_gradient(lsopc_plan* plan, const lsopc_kset* ks, const double* ma
     check_kset(plan, ks);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t n = plan->n();
-    plan->A.ensure((size_t)ks->nk * n * plan->g.csize());
-    launch_mask_fft(plan->g, nullptr, mask_dev, plan->mhat.p, plan->scratch.p, nullptr, s);
+    launch_mask_fft(plan->g, nullptr, mask_dev, nullptr, plan->mhat.p, plan->scratch.p, nullptr, s);
     ck_launch("mask fft");
-    forward(plan, ks, plan->If.p, plan->A.p, nullptr, s);
+    forward(plan, ks, nullptr, nullptr, s);
     launch_gate(plan->g, z_dev, zt_dev, 1.0, plan->wf.p, s);
     ck_launch("gate");
-    launch_adjoint_set(plan->g, ks->nk, plan->A.p, plan->wf.p, ks->spec.p, ks->w.data(), plan->G.p, true,
-                       plan->scratch.p, nullptr, s);
+    SpecSet set = spec_set(plan, ks, 0, 0);
+    launch_adjoint(plan->g, &set, 1, nullptr, s);
     ck_launch("adjoint");
-    launch_adjoint_finish(plan->g, plan->G.p, 4.0 * sigma_z * dose / (double)n, out_dev, nullptr, nullptr,
-                          plan->scratch.p, nullptr, s);
+    launch_adjoint_finish(plan->g, plan->V0.p, nullptr, 4.0 * sigma_z * dose / (double)n, out_dev, nullptr,
+                          nullptr, nullptr, s);
     ck_launch("adjoint finish");
   });
 }
@@ -314,12 +333,9 @@ int lsopc_convolve(lsopc_plan* plan, const lsopc_kset* ks, const double* mask_de
     check_plan(plan);
     check_kset(plan, ks);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    plan->A.ensure((size_t)ks->nk * plan->n() * plan->g.csize());
-    launch_mask_fft(plan->g, nullptr, mask_dev, plan->mhat.p, plan->scratch.p, nullptr, s);
+    launch_mask_fft(plan->g, nullptr, mask_dev, nullptr, plan->mhat.p, plan->scratch.p, nullptr, s);
     ck_launch("mask fft");
-    forward(plan, ks, plan->If.p, plan->A.p, nullptr, s);
-    launch_to_c128(plan->g, plan->A.p, out_c128_dev, s);
-    ck_launch("convert");
+    forward(plan, ks, nullptr, nullptr, s, out_c128_dev);
   });
 }
 
@@ -408,7 +424,10 @@ struct lsopc_session {
 
 namespace {
 
-void enqueue_iteration(lsopc_session* ss, int it) {
+// Pass boundaries inside one iteration, for per-pass CUDA-event timing.
+enum { PS_MASK = 0, PS_F1, PS_F2, PS_RESIST, PS_A1, PS_A2, PS_A3, PS_LS, PS_N };
+
+void enqueue_iteration(lsopc_session* ss, int it, cudaEvent_t* ev = nullptr) {
   lsopc_plan* p = ss->plan;
   const Grid& g = p->g;
   const size_t n = g.n();
@@ -420,27 +439,34 @@ void enqueue_iteration(lsopc_session* ss, int it) {
   double* vprev = ss->v[(it + 1) & 1].as<double>();
   double* d = ss->d[it & 1].as<double>();
   double* dprev = ss->d[(it + 1) & 1].as<double>();
-  const size_t fbytes = (size_t)ss->focus->nk * n * g.csize();
-  void* A_f = p->A.p;
-  void* A_d = static_cast<char*>(p->A.p) + fbytes;
+  auto mark = [&](int i) {
+    if (ev) cudaEventRecord(ev[i], s);
+  };
+  SpecSet sets[2] = {spec_set(p, ss->focus, 0, 0), spec_set(p, ss->defocus, 1, ss->focus->nk)};
 
-  // forward: M^ -> fields at the focus and defocus sets -> resist, losses, gates
-  launch_mask_fft(g, ss->mask.as<uint8_t>(), nullptr, p->mhat.p, p->scratch.p, stop, s);
-  forward(p, ss->focus, p->If.p, A_f, stop, s);
-  forward(p, ss->defocus, p->Id.p, A_d, stop, s);
+  // forward: M^ -> T_k -> I_f, I_d -> resist, losses, gates
+  mark(0);
+  launch_mask_fft(g, ss->mask.as<uint8_t>(), nullptr, nullptr, p->mhat.p, p->scratch.p, stop, s);
+  mark(1);
+  launch_f1(g, p->mhat.p, sets, 2, stop, s);
+  mark(2);
+  launch_f2(g, sets, 2, nullptr, stop, s);
+  mark(3);
   ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
   launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr, nullptr,
                 nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s);
   LoopCfg lc{c.alpha, c.beta, c.stop_rel_tol, c.stop_patience};
   launch_after_forward(p->partials.as<double>(), reduce_blocks(), lc, it, st, ss->hist.as<double>(), s);
   launch_copy_best(n, ss->phi.as<double>(), ss->best.as<double>(), st, s);
-  // adjoint: one frequency-domain accumulator for both sets, one inverse
-  launch_adjoint_set(g, ss->focus->nk, A_f, p->wf.p, ss->focus->spec.p, ss->focus->w.data(), p->G.p, true,
-                     p->scratch.p, stop, s);
-  launch_adjoint_set(g, ss->defocus->nk, A_d, p->wd.p, ss->defocus->spec.p, ss->defocus->w.data(), p->G.p, false,
-                     p->scratch.p, stop, s);
-  int ndots = launch_adjoint_finish(g, p->G.p, 4.0 * c.sigma_z / (double)n, v, it > 0 ? vprev : nullptr,
-                                    ss->dots.as<double>(), p->scratch.p, stop, s);
+  mark(4);
+  // adjoint: U_k, then one frequency-domain accumulator per set and one inverse
+  launch_a1(g, sets, 2, stop, s);
+  mark(5);
+  launch_a2(g, sets, 2, stop, s);
+  mark(6);
+  int ndots = launch_adjoint_finish(g, p->V0.p, p->V1.p, 4.0 * c.sigma_z / (double)n, v, it > 0 ? vprev : nullptr,
+                                    ss->dots.as<double>(), stop, s);
+  mark(7);
   const int restart = (it % c.cg_restart_every == 0) ? 1 : 0;
   launch_after_grad(ss->dots.as<double>(), ndots, restart || it == 0, st, s);
   // level-set step
@@ -452,6 +478,7 @@ void enqueue_iteration(lsopc_session* ss, int it) {
                    c.d_lower, c.d_upper, st, ss->mask.as<uint8_t>(),
                    ss->part_up.as<double>(), s);
   launch_after_update(ss->part_up.as<double>(), ls_blocks(), st, ss->hist.as<double>(), s);
+  mark(8);
   ck_launch("dso iteration");
 }
 
@@ -494,8 +521,8 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
       ss->state.ensure(sizeof(DevState));
       ss->part_ls.ensure((size_t)ls_blocks() * 2 * sizeof(double));
       ss->part_up.ensure((size_t)ls_blocks() * sizeof(double));
-      ss->dots.ensure((size_t)g.H * 2 * sizeof(double));
-      plan->A.ensure((size_t)(focus->nk + defocus->nk) * n * g.csize());
+      ss->dots.ensure((size_t)(finish_max_blocks() + 1) * 2 * sizeof(double));
+      plan->ensure_T(focus->nk + defocus->nk);
       // optimizer.py:197-201: uniform target -> DegenerateInputError
       {
         DevBuf zero;
@@ -572,9 +599,8 @@ int lsopc_session_finish(lsopc_session* ss, double* best_phi_dev, uint8_t* final
     // optimizer.py:271-277: best phi -> mask -> hard corners -> L2 / PVB
     uint8_t* fm = final_mask_dev ? final_mask_dev : ss->mask.as<uint8_t>();
     launch_elementwise(EW_MASK, n, ss->best.as<double>(), nullptr, 0, 0, 0, nullptr, fm, s);
-    launch_mask_fft(g, fm, nullptr, p->mhat.p, p->scratch.p, nullptr, s);
-    forward(p, ss->focus, p->If.p, nullptr, nullptr, s);
-    forward(p, ss->defocus, p->Id.p, nullptr, nullptr, s);
+    launch_mask_fft(g, fm, nullptr, nullptr, p->mhat.p, p->scratch.p, nullptr, s);
+    forward(p, ss->focus, ss->defocus, nullptr, s);
     uint8_t* hn = p->hard.as<uint8_t>();
     ResistParams rp{ss->cfg.i_th, ss->cfg.sigma_z, 0.0, 0.0};
     launch_resist(g, p->If.p, p->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr, nullptr, hn, hn + n,
@@ -607,26 +633,32 @@ int lsopc_session_destroy(lsopc_session* ss) {
   });
 }
 
-int lsopc_bench_pass(lsopc_plan* plan, const lsopc_kset* ks, int which, int reps, void* stream) {
+int lsopc_session_time_passes(lsopc_session* ss, int reps, double* ms_out) {
   return guarded([&] {
-    check_plan(plan);
-    check_kset(plan, ks);
-    if (which < 0 || which > 3) throw Error(LSOPC_EINVAL, "bad pass id");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    plan->A.ensure(plan->n() * plan->g.csize());
-    for (int r = 0; r < reps; ++r)
-      launch_bench_pass(plan->g, which, ks->spec.p, plan->mhat.p, plan->A.p, plan->If.p, plan->wf.p, plan->G.p,
-                        plan->scratch.p, s);
-    ck_launch("bench pass");
+    if (!ss) throw Error(LSOPC_EINVAL, "null session");
+    if (reps < 1) throw Error(LSOPC_EINVAL, "reps must be >= 1");
+    cudaEvent_t ev[PS_N + 1];
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    double acc[PS_N] = {0};
+    for (int r = 0; r < reps && ss->it < ss->cfg.max_iters; ++r) {
+      enqueue_iteration(ss, ss->it++, ev);
+      ck(cudaEventSynchronize(ev[PS_N]), "sync");
+      for (int i = 0; i < PS_N; ++i) {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]), "elapsed");
+        acc[i] += ms;
+      }
+    }
+    for (int i = 0; i < PS_N; ++i) ms_out[i] = acc[i] / reps;
+    for (auto& e : ev) cudaEventDestroy(e);
   });
 }
 
 int lsopc_session_launches_per_iter(const lsopc_session* ss) {
   if (!ss) return 0;
-  // mask fft 2, forward 2 per kernel, resist+after 2, copy 1, adjoint 2 per kernel,
-  // finish 2, after_grad 1, velocity+after 2, update+after 2
-  const int nk = ss->focus->nk + ss->defocus->nk;
-  return 2 + 2 * nk + 2 + 1 + 2 * nk + 2 + 1 + 2 + 2;
+  // mask rows+cols 2, F1 1, F2 1, resist 1, after_forward 1, copy_best 1, A1 1, A2 1,
+  // A3 1, after_grad 1, velocity+after 2, update+after 2
+  return 2 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 2 + 2;
 }
 
 int lsopc_optimize(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_kset* defocus, const uint8_t* target_dev,

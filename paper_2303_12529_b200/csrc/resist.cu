@@ -1,0 +1,119 @@
+// Resist model, losses and adjoint gates (pointwise, grid-stride).
+//
+// Replaces (reference, /root/reference/pkg/src/lsopc):
+//   resist_sigmoid / resist_hard               litho.py:129-138
+//   corner doses (nominal / outer / inner)     litho.py:98-100,147-149
+//   ilt_loss / pvb_loss                        optimizer.py:88-96
+//   the adjoint gate (Z - Z_t) Z (1 - Z)       optimizer.py:109, 114-134
+#include "common.cuh"
+#include "internal.h"
+
+namespace lsb {
+
+namespace {
+
+// ---- resist / losses / gates -------------------------------------------------
+
+constexpr int kRedBlocks = 148 * 4;
+constexpr int kRedThreads = 256;
+
+LS_D double sigmoid(double i, double i_th, double sz) { return 1.0 / (1.0 + exp(-sz * (i - i_th))); }
+
+template <typename R>
+__global__ void __launch_bounds__(kRedThreads)
+k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uint8_t* __restrict__ tu8,
+         const double* __restrict__ tf, ResistParams p, R* wf, R* wd, double* z_nom, double* z_in,
+         double* z_out, uint8_t* h_nom, uint8_t* h_in, uint8_t* h_out, double* partials,
+         StopFlag stop) {
+  __shared__ double red[64];
+  if (stop && *stop) return;
+  double acc[2] = {0.0, 0.0};
+  const bool have_t = tu8 || tf;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    // litho.py:125-126: I = max(dose * sum, 0); corners: litho.py:147-149
+    double sf = (double)If[i];
+    double i_nom = fmax(1.0 * sf, 0.0);
+    double i_out = fmax(1.02 * sf, 0.0);
+    double i_in = Id ? fmax(0.98 * (double)Id[i], 0.0) : 0.0;
+    if (h_nom) {  // litho.py:129-131 (inclusive threshold)
+      h_nom[i] = i_nom >= p.i_th;
+      h_out[i] = i_out >= p.i_th;
+      if (h_in) h_in[i] = i_in >= p.i_th;
+    }
+    if (!z_nom && !wf && !partials) continue;
+    double zn = sigmoid(i_nom, p.i_th, p.sigma_z);
+    double zo = sigmoid(i_out, p.i_th, p.sigma_z);
+    double zi = sigmoid(i_in, p.i_th, p.sigma_z);
+    if (z_nom) {
+      z_nom[i] = zn;
+      z_out[i] = zo;
+      if (z_in) z_in[i] = zi;
+    }
+    if (have_t) {
+      double zt = tu8 ? (double)tu8[i] : tf[i];
+      double dn = zn - zt, di = zi - zt, dout = zo - zt;
+      acc[0] += dn * dn;               // optimizer.py:88-90
+      acc[1] += di * di + dout * dout;  // optimizer.py:93-96
+      if (wf) {
+        // optimizer.py:109 gate, 114-134 doses and alpha/beta folded per kernel set
+        double gn = dn * zn * (1.0 - zn);
+        double go = dout * zo * (1.0 - zo);
+        double gi = di * zi * (1.0 - zi);
+        wf[i] = (R)(p.alpha * gn + p.beta * 1.02 * go);
+        wd[i] = (R)(p.beta * 0.98 * gi);
+      }
+    }
+  }
+  if (partials) {
+    block_sum<2>(acc, red);
+    if (threadIdx.x == 0) {
+      partials[2 * blockIdx.x] = acc[0];
+      partials[2 * blockIdx.x + 1] = acc[1];
+    }
+  }
+}
+
+template <typename R>
+__global__ void k_scale_intensity(size_t n, const R* __restrict__ I, double dose, double* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = fmax(dose * (double)I[i], 0.0);
+}
+
+template <typename R>
+__global__ void k_gate(size_t n, const double* __restrict__ z, const double* __restrict__ zt, double scale,
+                       R* w) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    double zz = z[i];
+    w[i] = (R)(scale * ((zz - zt[i]) * zz * (1.0 - zz)));
+  }
+}
+
+}  // namespace
+
+int reduce_blocks() { return kRedBlocks; }
+
+void launch_resist(const Grid& g, const void* If, const void* Id, const uint8_t* tu8, const double* tf,
+                   ResistParams p, void* wf, void* wd, double* z_nom, double* z_in, double* z_out,
+                   uint8_t* h_nom, uint8_t* h_in, uint8_t* h_out, double* partials, StopFlag stop,
+                   cudaStream_t s) {
+  if (g.prec == F64)
+    k_resist<double><<<kRedBlocks, kRedThreads, 0, s>>>(
+        g.n(), static_cast<const double*>(If), static_cast<const double*>(Id), tu8, tf, p,
+        static_cast<double*>(wf), static_cast<double*>(wd), z_nom, z_in, z_out, h_nom, h_in, h_out, partials, stop);
+  else
+    k_resist<float><<<kRedBlocks, kRedThreads, 0, s>>>(
+        g.n(), static_cast<const float*>(If), static_cast<const float*>(Id), tu8, tf, p,
+        static_cast<float*>(wf), static_cast<float*>(wd), z_nom, z_in, z_out, h_nom, h_in, h_out, partials, stop);
+}
+
+void launch_scale_intensity(const Grid& g, const void* I, double dose, double* out, cudaStream_t s) {
+  if (g.prec == F64) k_scale_intensity<double><<<kRedBlocks, 256, 0, s>>>(g.n(), static_cast<const double*>(I), dose, out);
+  else k_scale_intensity<float><<<kRedBlocks, 256, 0, s>>>(g.n(), static_cast<const float*>(I), dose, out);
+}
+
+void launch_gate(const Grid& g, const double* z, const double* zt, double scale, void* w, cudaStream_t s) {
+  if (g.prec == F64) k_gate<double><<<kRedBlocks, 256, 0, s>>>(g.n(), z, zt, scale, static_cast<double*>(w));
+  else k_gate<float><<<kRedBlocks, 256, 0, s>>>(g.n(), z, zt, scale, static_cast<float*>(w));
+}
+
+}  // namespace lsb
