@@ -165,8 +165,8 @@ def algorithmic_bytes_per_iter(n, n_k_total, prec):
 
 
 PASS_NAMES = ["mask_fft (rows+cols)", "F1 forward cols: T_k = IFFT_y(M^.H_k)",
-              "F2 forward rows: I = sum w|IFFT_x T_k|^2", "resist/loss/best",
-              "A1 adjoint rows: U_k = FFT_x(gate.IFFT_x T_k)",
+              "F2 forward rows: A_k = IFFT_x T_k, I = sum w|A_k|^2", "resist/loss/best",
+              "A1 adjoint rows: U_k = FFT_x(gate.A_k)",
               "A2 adjoint cols: V = IFFT_y(sum w conj(H_k).FFT_y U_k)", "A3 finish: g = Re IFFT_x V (+CG dots)",
               "level-set step (velocity, CFL, update)"]
 
@@ -178,9 +178,9 @@ def pass_bytes(n, nk_tot, nsets, prec):
     r = 4 if prec == "fp32" else 8
     per_px = [1 + 4 * c,                       # u8 mask in, M~ out+in, M^ out
               nk_tot * 2 * c + nsets * c,      # H_k in, T_k out; M^ tile once per (tile, set)
-              nk_tot * c + nsets * r,          # T_k in; I_set out
+              nk_tot * 2 * c + nsets * r,      # T_k in, A_k out; I_set out
               4 * r + 1,                       # I_f, I_d in; gates out; target in
-              nk_tot * 2 * c + nsets * r,      # T_k in, U_k out; gate once per (block, set)
+              nk_tot * 2 * c + nsets * r,      # A_k in, U_k out; gate once per (block, set)
               nk_tot * 2 * c + nsets * c,      # U_k in, H_k in; V_set out
               2 * c + 24,                      # V_f, V_d in; v out; v_prev in (dots)
               73]                              # phi stencil, v, d_prev, m in; d, u out; phi, mask out

@@ -139,9 +139,12 @@ LS_HD int stage_bits(int lgn, int lgp, int s) {
 }
 
 // One radix-RAD Stockham stage over the buffer's S sequences.  FIRST reads
-// through f.load(seq, idx); LAST writes through f.store(seq, idx, value, slot)
-// where slot = i*RAD + r is stable per thread across calls of the same
-// geometry (accumulators can live in registers).  Inverse transforms use
+// through f.load<STRIDE>(seq, j, r) and LAST writes through
+// f.store<STRIDE>(seq, j, r, value, slot), both for index idx = j + r*STRIDE
+// (STRIDE is a compile-time constant on the fast path, 0 = "j is the index"
+// on the generic path), so functors can fold addresses to base + r*const.
+// slot = i*RAD + r is stable per thread across calls of the same geometry
+// (accumulators can live in registers).  Inverse transforms use
 // conj(FFT(conj x)), unnormalised.  The read and write phases of every stage
 // are separated by a barrier, so load/store functors may use the buffer
 // itself (in-place).
@@ -166,7 +169,7 @@ LS_D void stage(C (&v)[P_of<C>()], const Geo& g, int lgNs, C* sm, const C* __res
       const int idx = j + r * nr;
       C x;
       if constexpr (FIRST) {
-        x = f.load(seq, idx);
+        x = f.template load<0>(seq, idx, 0);
         if constexpr (INV) x = cconj(x);
       } else {
         x = sm[xaddr<C, COLS>(seq, idx, g.lgS, ld)];
@@ -195,7 +198,7 @@ LS_D void stage(C (&v)[P_of<C>()], const Geo& g, int lgNs, C* sm, const C* __res
       C x = v[i * RAD + r];
       if constexpr (LAST) {
         if constexpr (INV) x = cconj(x);
-        f.store(seq, idx, x, i * RAD + r);
+        f.template store<0>(seq, idx, 0, x, i * RAD + r);
       } else {
         sm[xaddr<C, COLS>(seq, idx, g.lgS, ld)] = x;
       }
@@ -329,7 +332,7 @@ LS_D void stage_t(C (&v)[P_of<C>()], C* sm, const C* __restrict__ tw, int tws, F
     for (int r = 0; r < RAD; ++r) {
       C x;
       if constexpr (FIRST) {
-        x = f.load(seq, j + r * nr);
+        x = f.template load<nr>(seq, j, r);
         if constexpr (INV) x = cconj(x);
       } else {
         x = sm[xaddr_t<C, COLS, LGS, LD, nr>(seq, j, r)];
@@ -355,7 +358,7 @@ LS_D void stage_t(C (&v)[P_of<C>()], C* sm, const C* __restrict__ tw, int tws, F
       C x = v[i * RAD + r];
       if constexpr (LAST) {
         if constexpr (INV) x = cconj(x);
-        f.store(seq, base + r * Ns, x, i * RAD + r);
+        f.template store<Ns>(seq, base, r, x, i * RAD + r);
       } else {
         sm[xaddr_t<C, COLS, LGS, LD, Ns>(seq, base, r)] = x;
       }
@@ -389,39 +392,67 @@ LS_D void last_pos_t(int slot, int& seq, int& idx) {
   idx = j + r * nr;
 }
 
-// Dispatch: compile-time geometry when the buffer is full and n >= 256,
-// otherwise the runtime-geometry path (small test grids).
-#define ENG_FAST_CASES(X) X(8) X(9) X(10) X(11) X(12) X(13)
+// Compile-time geometry handle passed to op bodies: LGN > 0 on the fast path
+// (LGS = log2(512 P) - LGN), LGN == 0 on the runtime-geometry path.
+template <int LGN_> struct Fix { static constexpr int LGN = LGN_; };
 
-template <bool COLS, bool INV, typename C, class F>
-LS_D void run_any(const Geo& g, C* sm, const C* __restrict__ tw, F& f) {
+// Calls body(Fix<LGN>{}) once with the geometry folded to constants when the
+// buffer is full and n >= 256 (every production size), else body(Fix<0>{}).
+#define ENG_FAST_CASES(X) X(8) X(9) X(10) X(11) X(12) X(13)
+template <typename C, class Body>
+LS_D void dispatch(const Geo& g, bool allow, Body&& body) {
   constexpr int LGE = lg_full<C>();
-  if (g.lgS == LGE - g.lgn && g.lgn >= kFastMinLgn) {
-    C v[P_of<C>()];
+  if (allow && g.lgS == LGE - g.lgn && g.lgn >= kFastMinLgn) {
     switch (g.lgn) {
 #define ENG_CASE(L) \
-  case L: if constexpr (L <= LGE) run_stages<L, LGE - L, 0, COLS, INV>(v, sm, tw, g.tws, f); return;
+  case L: if constexpr (L <= LGE) { body(Fix<L>{}); return; } break;
       ENG_FAST_CASES(ENG_CASE)
 #undef ENG_CASE
       default: break;
     }
   }
-  run<COLS, INV>(g, sm, tw, f);
+  body(Fix<0>{});
 }
 
-template <bool COLS, typename C>
-LS_D void last_pos_any(const Geo& g, int slot, int& seq, int& idx) {
-  constexpr int LGE = lg_full<C>();
-  if (g.lgS == LGE - g.lgn && g.lgn >= kFastMinLgn) {
-    switch (g.lgn) {
-#define ENG_CASE(L) \
-  case L: if constexpr (L <= LGE) { last_pos_t<L, LGE - L, COLS, C>(slot, seq, idx); return; } break;
-      ENG_FAST_CASES(ENG_CASE)
-#undef ENG_CASE
-      default: break;
+// Run the transform with the geometry chosen by dispatch().
+template <int LGN, bool COLS, bool INV, typename C, class F>
+LS_D void run_fix(const Geo& g, C* sm, const C* __restrict__ tw, F& f) {
+  if constexpr (LGN > 0) {
+    C v[P_of<C>()];
+    run_stages<LGN, lg_full<C>() - LGN, 0, COLS, INV>(v, sm, tw, g.tws, f);
+  } else {
+    run<COLS, INV>(g, sm, tw, f);
+  }
+}
+
+// Calls fn(seq, j, r, slot) for every slot this thread owns in the LAST
+// stage (idx = j + r*STRIDE with STRIDE passed as a template argument of fn's
+// call operator via Fix-like constant).  Mirrors stage_t / stage exactly.
+template <int LGN, bool COLS, typename C, class Fn>
+LS_D void for_last_slots(const Geo& g, Fn&& fn) {
+  constexpr int P = P_of<C>();
+  if constexpr (LGN > 0) {
+    using PL = StagePlan<LGN, LGP_of<C>()>;
+    constexpr int LGR = PL::bits(PL::nst - 1), RAD = 1 << LGR, nr = (1 << LGN) >> LGR;
+    constexpr int LGS = lg_full<C>() - LGN;
+    constexpr int NT = ((1 << LGN) << LGS) / P;
+#pragma unroll
+    for (int i = 0; i < P / RAD; ++i) {
+      const int b = threadIdx.x + i * NT;
+      int seq, j;
+      if constexpr (COLS) { seq = b & ((1 << LGS) - 1); j = b >> LGS; }
+      else { j = b & (nr - 1); seq = b >> (LGN - LGR); }
+#pragma unroll
+      for (int r = 0; r < RAD; ++r) fn.template operator()<nr>(seq, j, r, i * RAD + r);
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      int seq, idx;
+      last_pos<COLS, C>(g, s, seq, idx);
+      fn.template operator()<0>(seq, idx, 0, s);
     }
   }
-  last_pos<COLS, C>(g, slot, seq, idx);
 }
 
 // ---- layouts -----------------------------------------------------------------
@@ -459,6 +490,52 @@ template <int ES> constexpr int lg_es() { return ES == 1 ? 0 : ES == 2 ? 1 : ES 
 template <int ES>
 LS_D void gather_rect(void* dst, const void* src, Lay L, int y0, int lgny, int x0, int lgnx) {
   constexpr int LGES = lg_es<ES>();
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  const int nt = blockDim.x;
+  // (a) the rectangle is whole tiles of full tile width (column items, or a
+  //     row-major source): each tile chunk of ny*w elements is contiguous.
+  if (lgnx >= L.lgw && L.lgw + LGES >= 4) {
+    const int lgw = L.lgw;
+    const int lgppt = lgny + lgw + LGES - 4;          // 16 B pieces per tile chunk
+    const int total = 1 << (lgnx - lgw + lgppt);
+    if (lgnx == lgw) {                                // single tile: plain copy
+      const char* s0 = s + ((L.at(y0, x0)) << LGES);
+      for (int p = threadIdx.x; p < total; p += nt) cp16(d + ((size_t)p << 4), s0 + ((size_t)p << 4));
+      return;
+    }
+    if (nt >= (1 << lgppt)) {                         // each thread keeps its offset inside a chunk
+      const int rem = threadIdx.x & ((1 << lgppt) - 1);
+      const int e = rem << (4 - LGES);                // element offset inside the chunk
+      const int r = e >> lgw, c = e & ((1 << lgw) - 1);
+      int t = threadIdx.x >> lgppt;
+      const int tstep = nt >> lgppt;
+      const char* sp = s + ((L.at(y0 + r, x0 + (t << lgw) + c)) << LGES);
+      char* dp = d + ((((size_t)r << lgnx) + (t << lgw) + c) << LGES);
+      const size_t sstride = ((size_t)tstep * L.H) << (lgw + LGES);
+      const size_t dstride = (size_t)tstep << (lgw + LGES);
+      for (int p = threadIdx.x; p < total; p += nt) {
+        cp16(dp, sp);
+        sp += sstride;
+        dp += dstride;
+      }
+      return;
+    }
+  }
+  // (b) a slab narrower than one tile (column items of a wider tiling): one
+  //     contiguous row segment of nx elements per row, 16 B pieces
+  if (lgnx < L.lgw && lgnx + LGES >= 4) {
+    const int lgprs = lgnx + LGES - 4;                // pieces per row segment
+    const int total = 1 << (lgny + lgprs);
+    const char* s0 = s + ((L.at(y0, x0)) << LGES);
+    const int lgrow = L.lgw + LGES;                   // bytes per tile row
+    for (int p = threadIdx.x; p < total; p += nt) {
+      const int r = p >> lgprs, cc = p & ((1 << lgprs) - 1);
+      cp16(d + ((size_t)p << 4), s0 + ((size_t)r << lgrow) + (cc << 4));
+    }
+    return;
+  }
+  // (c) general: pieces in source-address order (tile, row, chunk)
   const int lgwc = lgnx < L.lgw ? lgnx : L.lgw;      // columns per tile chunk
   int lgpb = lgwc + LGES;                            // bytes per contiguous row segment
   lgpb = lgpb > 4 ? 4 : lgpb;
@@ -466,9 +543,7 @@ LS_D void gather_rect(void* dst, const void* src, Lay L, int y0, int lgny, int x
   const int lgprs = lgwc - lgepp;                    // pieces per row segment
   const int lgppt = lgny + lgprs;                    // pieces per tile chunk
   const int total = 1 << (lgnx - lgwc + lgppt);
-  const char* s = static_cast<const char*>(src);
-  char* d = static_cast<char*>(dst);
-  for (int p = threadIdx.x; p < total; p += blockDim.x) {
+  for (int p = threadIdx.x; p < total; p += nt) {
     const int t = p >> lgppt, rem = p & ((1 << lgppt) - 1);
     const int r = rem >> lgprs, c = ((rem & ((1 << lgprs) - 1)) << lgepp) + (t << lgwc);
     const size_t so = L.at(y0 + r, x0 + c) << LGES;

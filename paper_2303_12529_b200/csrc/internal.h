@@ -36,7 +36,8 @@ struct SpecSet {
   int nk;
   const double* w;   // host weights (sigma_k), nk
   const void* spec;  // nk spectra
-  void* T;           // nk work fields: T_k after the forward, U_k after A1
+  void* T;           // nk column-tiled work fields: T_k after F1, U_k after A1
+  void* A;           // nk row-major fields A_k (F2 -> A1)
   void* I;           // real intensity sum_k w_k |A_k|^2, row-major (element R)
   const void* gate;  // real gate, row-major (element R)
   void* V;           // complex adjoint accumulator (column-tiled)

@@ -72,14 +72,18 @@ struct lsopc_plan {
   Grid g{};
   // T: per-kernel work fields (T_k / U_k) of the spectral passes, grown to the
   // largest (focus + defocus) kernel count used on this plan.
-  DevBuf tw, tw64, mhat, scratch, scratch2, T, V0, V1, If, Id, wf, wd, partials, scal, hard, tsdf_i, tsdf_f;
+  // A: per-kernel row-major fields A_k (F2 -> A1).
+  DevBuf tw, tw64, mhat, scratch, scratch2, T, A, V0, V1, If, Id, wf, wd, partials, scal, hard, tsdf_i, tsdf_f;
   ~lsopc_plan() {
-    for (DevBuf* b : {&tw, &tw64, &mhat, &scratch, &scratch2, &T, &V0, &V1, &If, &Id, &wf, &wd, &partials, &scal,
-                      &hard, &tsdf_i, &tsdf_f})
+    for (DevBuf* b : {&tw, &tw64, &mhat, &scratch, &scratch2, &T, &A, &V0, &V1, &If, &Id, &wf, &wd, &partials,
+                      &scal, &hard, &tsdf_i, &tsdf_f})
       b->release();
   }
   size_t n() const { return g.n(); }
-  void ensure_T(int nk_total) { T.ensure((size_t)nk_total * n() * g.csize()); }
+  void ensure_T(int nk_total) {
+    T.ensure((size_t)nk_total * n() * g.csize());
+    A.ensure((size_t)nk_total * n() * g.csize());
+  }
 };
 
 struct lsopc_kset {
@@ -128,6 +132,7 @@ SpecSet spec_set(lsopc_plan* p, const lsopc_kset* ks, int which, size_t T_off_ke
   s.w = ks->w.data();
   s.spec = ks->spec.p;
   s.T = static_cast<char*>(p->T.p) + T_off_kernels * p->n() * p->g.csize();
+  s.A = static_cast<char*>(p->A.p) + T_off_kernels * p->n() * p->g.csize();
   s.I = which == 0 ? p->If.p : p->Id.p;
   s.gate = which == 0 ? p->wf.p : p->wd.p;
   s.V = which == 0 ? p->V0.p : p->V1.p;

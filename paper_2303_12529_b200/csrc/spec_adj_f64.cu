@@ -1,0 +1,11 @@
+// Explicit instantiations of the adj spectral passes for double (parallel build units).
+#include "spectral.cuh"
+
+namespace lsb {
+namespace spec {
+template void a1_impl<double>(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
+template void a2_impl<double>(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
+template int finish_impl<double>(const Grid& g, const void* V0, const void* V1, double scale, double* out, const double* vp,
+                double* dots, StopFlag stop, cudaStream_t s);
+}  // namespace spec
+}  // namespace lsb
