@@ -169,7 +169,7 @@ LS_D void stage(C (&v)[P_of<C>()], const Geo& g, int lgNs, C* sm, const C* __res
       const int idx = j + r * nr;
       C x;
       if constexpr (FIRST) {
-        x = f.template load<0>(seq, idx, 0);
+        x = f.template load<0>(seq, idx, 0, i * RAD + r);
         if constexpr (INV) x = cconj(x);
       } else {
         x = sm[xaddr<C, COLS>(seq, idx, g.lgS, ld)];
@@ -332,7 +332,7 @@ LS_D void stage_t(C (&v)[P_of<C>()], C* sm, const C* __restrict__ tw, int tws, F
     for (int r = 0; r < RAD; ++r) {
       C x;
       if constexpr (FIRST) {
-        x = f.template load<nr>(seq, j, r);
+        x = f.template load<nr>(seq, j, r, i * RAD + r);
         if constexpr (INV) x = cconj(x);
       } else {
         x = sm[xaddr_t<C, COLS, LGS, LD, nr>(seq, j, r)];
@@ -422,6 +422,26 @@ LS_D void run_fix(const Geo& g, C* sm, const C* __restrict__ tw, F& f) {
     run_stages<LGN, lg_full<C>() - LGN, 0, COLS, INV>(v, sm, tw, g.tws, f);
   } else {
     run<COLS, INV>(g, sm, tw, f);
+  }
+}
+
+// Calls fn(seq, j, r, slot) for every slot this thread reads in the FIRST
+// stage (the load functor's arguments), fast path only.
+template <int LGN, bool COLS, typename C, class Fn>
+LS_D void for_first_slots(Fn&& fn) {
+  constexpr int P = P_of<C>();
+  using PL = StagePlan<LGN, LGP_of<C>()>;
+  constexpr int LGR = PL::bits(0), RAD = 1 << LGR, nr = (1 << LGN) >> LGR;
+  constexpr int LGS = lg_full<C>() - LGN;
+  constexpr int NT = ((1 << LGN) << LGS) / P;
+#pragma unroll
+  for (int i = 0; i < P / RAD; ++i) {
+    const int b = threadIdx.x + i * NT;
+    int seq, j;
+    if constexpr (COLS) { seq = b & ((1 << LGS) - 1); j = b >> LGS; }
+    else { j = b & (nr - 1); seq = b >> (LGN - LGR); }
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) fn.template operator()<nr>(seq, j, r, i * RAD + r);
   }
 }
 

@@ -42,22 +42,26 @@ using eng::Geo;
 using eng::Lay;
 
 constexpr int kMaxK = 64;  // kernels per set carried in a launch
-// Tile width of the column-tiled layout: 8 elements, so a 4-row item (FP32) or
-// 2-row item (FP64) reads 256 B chunks -- measured at full HBM bandwidth on B200,
-// against 73% for 128 B chunks (scripts/mb_layout.cu, profiles/).
-constexpr int kLgTile = 2;
+// Tile widths of the column-tiled layouts (scripts/mb_layout.cu measured on
+// B200: whole-tile column items stream at 6.2 TB/s; a 4-row item reads 128 B
+// chunks of a 4-wide tiling at 73% of that and 256 B chunks of an 8-wide
+// tiling at full speed, while a 4-column item of an 8-wide tiling runs at 91%).
+constexpr int kLgTile = 2;   // U_k, V, M^, spectra: column items read whole tiles
+constexpr int kLgTileT = 3;  // T_k: read by the F2 row pass as 256 B chunks
 
 template <typename R> struct Shape {
   int H, W, lgH, lgW;
   int lgS, lgR;     // log2 columns per column item / rows per row item
   int lgT;          // log2 tile width of the column-tiled layout (decoupled from lgS)
+  int lgTT;         // log2 tile width of the T_k fields
   int twsH, twsW;   // twiddle-table shifts for the two axes
   LS_HD Geo gcol() const { return Geo{lgH, lgS, twsH}; }
   LS_HD Geo grow() const { return Geo{lgW, lgR, twsW}; }
   LS_HD Lay ct() const { return Lay{H, lgT}; }   // column-tiled layout of spectral fields
   LS_HD Lay rm() const { return Lay{H, lgW}; }   // row-major
   // compile-time-geometry path allowed (layout tile width is the constant one)
-  LS_HD bool fast() const { return lgT == kLgTile; }
+  LS_HD bool fast() const { return lgT == kLgTile && lgTT == kLgTileT; }
+  LS_HD Lay ctT() const { return Lay{H, lgTT}; }  // layout of the T_k fields
 };
 
 template <typename R> Shape<R> shape_of(const Grid& g) {
@@ -68,6 +72,7 @@ template <typename R> Shape<R> shape_of(const Grid& g) {
   s.lgS = std::max(0, std::min(g.lgW, ilog2i(E) - g.lgH));
   s.lgR = std::max(0, std::min(g.lgH, ilog2i(E) - g.lgW));
   s.lgT = std::min(g.lgW, kLgTile);
+  s.lgTT = std::min(g.lgW, kLgTileT);
   s.twsH = g.lgnmax - g.lgH;
   s.twsW = g.lgnmax - g.lgW;
   return s;
@@ -89,40 +94,48 @@ __global__ void k_ct_to_c128(size_t n, Lay L, int W, const typename CT<R>::C* __
 template <typename R, class Op>
 __global__ void __launch_bounds__(512, 1) k_pass(Op op, StopFlag stop) {
   using C = typename CT<R>::C;
+  constexpr int NB = Op::kStages;  // ring of stage buffers: prefetch distance NB - 1
   if (stop && *stop) return;
   extern __shared__ __align__(16) unsigned char smraw[];
-  C* const b0 = reinterpret_cast<C*>(smraw);
-  C* const b1 = b0 + op.bufE;
-  C* extra = reinterpret_cast<C*>(smraw) + 2 * op.bufE;
+  C* const base = reinterpret_cast<C*>(smraw);
+  C* extra = base + NB * op.bufE;
   typename Op::State S{};
-  int it = blockIdx.x;
-  if (it >= op.nitems) return;
-  int st = 0, par = 0;
-  op.prefetch(it, 0, b0, extra);
-  eng::cp_commit();
-  while (true) {
-    int nit = it, nst = st + 1;
-    if (nst == op.steps(it)) { nst = 0; nit = it + gridDim.x; }
-    const bool more = nit < op.nitems;
-    if (more) op.prefetch(nit, nst, par ? b0 : b1, extra);
+  if ((int)blockIdx.x >= op.nitems) return;
+  // cursor over this CTA's flattened (item, step) sequence
+  auto advance = [&](int& it, int& st) {
+    if (++st == op.steps(it)) { st = 0; it += gridDim.x; }
+  };
+  int it = blockIdx.x, st = 0;
+  int pit = it, pst = st;  // next (item, step) to prefetch
+#pragma unroll
+  for (int d = 0; d < NB - 1; ++d) {
+    if (pit < op.nitems) op.prefetch(pit, pst, base + d * op.bufE, extra);
     eng::cp_commit();
-    eng::cp_wait<1>();
+    if (pit < op.nitems) advance(pit, pst);
+  }
+  int slot = 0;  // ring slot of (it, st)
+  while (true) {
+    const int pslot = slot == 0 ? NB - 1 : slot - 1;  // == (slot + NB - 1) % NB
+    if (pit < op.nitems) op.prefetch(pit, pst, base + pslot * op.bufE, extra);
+    eng::cp_commit();
+    eng::cp_wait<NB - 1>();
     __syncthreads();
-    C* const cur = par ? b1 : b0;
+    C* const cur = base + slot * op.bufE;
     if (st == 0) op.begin(S, it, extra);
     op.step(S, it, st, cur, extra);
     __syncthreads();
     if (st == op.steps(it) - 1) op.end(S, it, cur, extra);
-    if (!more) break;
-    it = nit;
-    st = nst;
-    par ^= 1;
+    if (pit < op.nitems) advance(pit, pst);
+    advance(it, st);
+    if (it >= op.nitems) break;
+    slot = slot == NB - 1 ? 0 : slot + 1;
   }
   op.finish(S, reinterpret_cast<double*>(smraw));
 }
 
 struct NoState {};
 struct OpBase {
+  static constexpr int kStages = 3;
   int bufE = 0, nitems = 0;
   LS_D int steps(int) const { return 1; }
   template <class S, class C> LS_D void begin(S&, int, C*) const {}
@@ -147,20 +160,20 @@ template <int LGN, int STRIDE> LS_D int nat_row(int seq, int j, int r, int lgn) 
   else return (seq << lgn) + j;
 }
 // column-tiled element (y = j + r*STRIDE, x); fast path has tile width 2^kLgTile
-template <int LGN, int STRIDE> LS_D size_t ct_col(const Lay& L, int j, int r, int x) {
+template <int LGN, int STRIDE, int LGT = kLgTile> LS_D size_t ct_col(const Lay& L, int j, int r, int x) {
   if constexpr (LGN > 0) {
-    constexpr int T = 1 << kLgTile;
-    return (((size_t)(x >> kLgTile) * L.H + j) << kLgTile) + (x & (T - 1)) + (size_t)r * (STRIDE << kLgTile);
+    constexpr int T = 1 << LGT;
+    return (((size_t)(x >> LGT) * L.H + j) << LGT) + (x & (T - 1)) + (size_t)r * (STRIDE << LGT);
   } else {
     return L.at(j, x);
   }
 }
 // column-tiled element (y, x = j + r*STRIDE)
-template <int LGN, int STRIDE> LS_D size_t ct_row(const Lay& L, int y, int j, int r) {
+template <int LGN, int STRIDE, int LGT = kLgTile> LS_D size_t ct_row(const Lay& L, int y, int j, int r) {
   if constexpr (LGN > 0) {
-    constexpr int T = 1 << kLgTile;
+    constexpr int T = 1 << LGT;
     static_assert(STRIDE % T == 0, "row stride must be a multiple of the tile width");
-    return (((size_t)(j >> kLgTile) * L.H + y) << kLgTile) + (j & (T - 1)) + (size_t)r * STRIDE * L.H;
+    return (((size_t)(j >> LGT) * L.H + y) << LGT) + (j & (T - 1)) + (size_t)r * STRIDE * L.H;
   } else {
     return L.at(y, j);
   }
@@ -193,7 +206,7 @@ template <typename R> struct MaskRowsOp : OpBase {
     int kind, y0, lgn;
     C* out;
     Lay L;
-    template <int ST> LS_D C load(int seq, int j, int r) const {
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const int p = nat_row<LGN, ST>(seq, j, r, lgn);
       R m;
       if (kind == SRC_U8) m = (R)raw[p];
@@ -237,7 +250,7 @@ template <typename R, typename RO, bool INV> struct ColsOp : OpBase {
     Lay L;
     int x0, lgS;
     R scale;
-    template <int ST> LS_D C load(int seq, int j, int r) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)] * scale; }
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)] * scale; }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
       out[ct_col<LGN, ST>(L, j, r, x0 + seq)] = cmk((RO)v.x, (RO)v.y);
     }
@@ -269,7 +282,7 @@ template <typename R, bool INV> struct RowsOp : OpBase {
     C* out;
     Lay L;
     int y0, lgn;
-    template <int ST> LS_D C load(int seq, int j, int r) const { return b[nat_row<LGN, ST>(seq, j, r, lgn)]; }
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_row<LGN, ST>(seq, j, r, lgn)]; }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[L.at(y0 + seq, j + r * ST)] = v; }
   };
   template <class St> LS_D void step(St&, int it, int, C* b, C*) const {
@@ -298,10 +311,11 @@ template <typename R> struct SetArgs {
   R w[2][kMaxK];         // kernel weights (sigma_k)
 };
 
-// F1: T_k = IFFT_y(M^ . H_k) / (HW)
+// F1: T_k = IFFT_y(M^ . H_k) / (HW); the item's M^ values stay in registers
 template <typename R> struct F1Op : OpBase {
   using C = typename CT<R>::C;
-  using State = NoState;
+  static constexpr int P = eng::P_of<C>();
+  struct State { C mh[P]; };
   Shape<R> sh;
   SetArgs<R> a;
   const C* mhat;
@@ -314,32 +328,45 @@ template <typename R> struct F1Op : OpBase {
     const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
     eng::gather_rect<sizeof(C)>(b, a.spec[set] + (size_t)k * fsz(), sh.ct(), 0, sh.lgH, t << sh.lgS, sh.lgS);
   }
-  LS_D void begin(State&, int it, C* mh) const {
+  template <int LGN> struct LoadM {
+    State& S;
+    const C* mhat;
+    Lay L;
+    int x0;
+    template <int ST> LS_D void operator()(int seq, int j, int r, int slot) const {
+      S.mh[slot] = __ldg(&mhat[ct_col<LGN, ST>(L, j, r, x0 + seq)]);
+    }
+  };
+  LS_D void begin(State& S, int it, C*) const {
     const int t = it & ((1 << lgnt) - 1);
-    eng::gather_rect<sizeof(C)>(mh, mhat, sh.ct(), 0, sh.lgH, t << sh.lgS, sh.lgS);
-    eng::cp_commit();
-    eng::cp_wait<0>();
-    __syncthreads();
+    eng::dispatch<C>(sh.gcol(), sh.fast(), [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) eng::for_first_slots<LGN, true, C>(LoadM<LGN>{S, mhat, sh.ct(), t << sh.lgS});
+    });
   }
   template <int LGN> struct F {
     const C* b;
-    const C* mh;
+    const State& S;
+    const C* mhat;  // generic path only
     C* out;
-    Lay L;
+    Lay L, Lm;
     int x0, lgS;
     R scale;
-    template <int ST> LS_D C load(int seq, int j, int r) const {
-      const int p = nat_col<LGN, ST, C>(seq, j, r, lgS);
-      return cmul(mh[p], b[p]) * scale;
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
+      const C x = b[nat_col<LGN, ST, C>(seq, j, r, lgS)];
+      if constexpr (LGN > 0) return cmul(S.mh[slot], x) * scale;
+      else return cmul(mhat[Lm.at(j, x0 + seq)], x) * scale;
     }
-    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_col<LGN, ST>(L, j, r, x0 + seq)] = v; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
+      out[ct_col<LGN, ST, kLgTileT>(L, j, r, x0 + seq)] = v;
+    }
   };
-  LS_D void step(State&, int it, int k, C* b, C* mh) const {
+  LS_D void step(State& S, int it, int k, C* b, C*) const {
     const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
     const Geo g = sh.gcol();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      F<LGN> f{b, mh, a.T[set] + (size_t)k * fsz(), sh.ct(), t << sh.lgS, sh.lgS, scale};
+      F<LGN> f{b, S, mhat, a.T[set] + (size_t)k * fsz(), sh.ctT(), sh.ct(), t << sh.lgS, sh.lgS, scale};
       eng::run_fix<LGN, true, true>(g, b, tw, f);
     });
   }
@@ -359,7 +386,7 @@ template <typename R> struct F2Op : OpBase {
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
   LS_D void prefetch(int it, int k, C* b, C*) const {
     const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
-    eng::gather_rect<sizeof(C)>(b, a.T[set] + (size_t)k * fsz(), sh.ct(), yb << sh.lgR, sh.lgR, 0, sh.lgW);
+    eng::gather_rect<sizeof(C)>(b, a.T[set] + (size_t)k * fsz(), sh.ctT(), yb << sh.lgR, sh.lgR, 0, sh.lgW);
   }
   LS_D void begin(State& S, int, C*) const {
 #pragma unroll
@@ -371,7 +398,7 @@ template <typename R> struct F2Op : OpBase {
     R w;
     C* A;  // row-major field k
     int y0, lgn, W;
-    template <int ST> LS_D C load(int seq, int j, int r) const { return b[nat_row<LGN, ST>(seq, j, r, lgn)]; }
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_row<LGN, ST>(seq, j, r, lgn)]; }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int slot) {
       S.acc[slot] += w * (v.x * v.x + v.y * v.y);
       A[rm_row<LGN, ST>(W, y0 + seq, j, r)] = v;
@@ -404,10 +431,12 @@ template <typename R> struct F2Op : OpBase {
   }
 };
 
-// A1: U_k = FFT_x(gate . A_k) -> column-tiled, over T_k
+// A1: U_k = FFT_x(gate . A_k) -> column-tiled, over T_k; the item's gate
+//     values stay in registers
 template <typename R> struct A1Op : OpBase {
   using C = typename CT<R>::C;
-  using State = NoState;
+  static constexpr int P = eng::P_of<C>();
+  struct State { R g[P]; };
   Shape<R> sh;
   SetArgs<R> a;
   const C* tw;
@@ -418,23 +447,41 @@ template <typename R> struct A1Op : OpBase {
     const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
     eng::gather_rect<sizeof(C)>(b, a.A[set] + (size_t)k * fsz(), sh.rm(), yb << sh.lgR, sh.lgR, 0, sh.lgW);
   }
+  template <int LGN> struct LoadG {
+    State& S;
+    const R* gate;
+    int y0, W;
+    template <int ST> LS_D void operator()(int seq, int j, int r, int slot) const {
+      S.g[slot] = __ldg(&gate[rm_row<LGN, ST>(W, y0 + seq, j, r)]);
+    }
+  };
+  LS_D void begin(State& S, int it, C*) const {
+    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    eng::dispatch<C>(sh.grow(), sh.fast(), [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) eng::for_first_slots<LGN, false, C>(LoadG<LGN>{S, a.gate[set], y0, sh.W});
+    });
+  }
   template <int LGN> struct F {
     const C* b;
-    const R* gate;
+    const State& S;
+    const R* gate;  // generic path only
     C* out;
     Lay L;
     int y0, lgn, W;
-    template <int ST> LS_D C load(int seq, int j, int r) const {
-      return b[nat_row<LGN, ST>(seq, j, r, lgn)] * __ldg(&gate[rm_row<LGN, ST>(W, y0 + seq, j, r)]);
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
+      const C x = b[nat_row<LGN, ST>(seq, j, r, lgn)];
+      if constexpr (LGN > 0) return x * S.g[slot];
+      else return x * gate[(size_t)(y0 + seq) * W + j];
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_row<LGN, ST>(L, y0 + seq, j, r)] = v; }
   };
-  LS_D void step(State&, int it, int k, C* b, C*) const {
+  LS_D void step(State& S, int it, int k, C* b, C*) const {
     const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
     const Geo g = sh.grow();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      F<LGN> f{b, a.gate[set], a.T[set] + (size_t)k * fsz(), sh.ct(), yb << sh.lgR, sh.lgW, sh.W};
+      F<LGN> f{b, S, a.gate[set], a.T[set] + (size_t)k * fsz(), sh.ct(), yb << sh.lgR, sh.lgW, sh.W};
       eng::run_fix<LGN, false, false>(g, b, tw, f);
     });
   }
@@ -474,7 +521,7 @@ template <typename R> struct A2Op : OpBase {
     const C (&h)[P];
     R w;
     int lgS;
-    template <int ST> LS_D C load(int seq, int j, int r) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)]; }
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)]; }
     template <int ST> LS_D void store(int, int, int, C v, int slot) { S.acc[slot] = S.acc[slot] + cmulc(v, h[slot]) * w; }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
@@ -501,7 +548,7 @@ template <typename R> struct A2Op : OpBase {
     C* out;
     Lay L;
     int x0, lgS;
-    template <int ST> LS_D C load(int seq, int j, int r) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)]; }
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)]; }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_col<LGN, ST>(L, j, r, x0 + seq)] = v; }
   };
   LS_D void end(State& S, int it, C* b, C*) const {
@@ -542,7 +589,7 @@ template <typename R> struct A3Op : OpBase {
     const double* vp;
     State& S;
     int y0, lgn, W;
-    template <int ST> LS_D C load(int seq, int j, int r) const {
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const C x = b[nat_row<LGN, ST>(seq, j, r, lgn)];
       return v1 ? x + __ldg(&v1[ct_row<LGN, ST>(L, y0 + seq, j, r)]) : x;
     }
@@ -593,7 +640,8 @@ inline int num_sms() {
 template <typename R, class Op>
 int launch_op(Op& op, int threads, int extra_bufs, StopFlag stop, cudaStream_t s, int max_grid = 0) {
   using C = typename CT<R>::C;
-  const size_t smem = std::max((size_t)(2 + extra_bufs) * op.bufE * sizeof(C), (size_t)(64 * sizeof(double)));
+  const size_t smem =
+      std::max((size_t)(Op::kStages + extra_bufs) * op.bufE * sizeof(C), (size_t)(64 * sizeof(double)));
   if (smem > 227 * 1024) throw std::runtime_error("spectral pass needs more than 227 KB of shared memory");
   auto kern = k_pass<R, Op>;
   static int per_sm = -1;
@@ -694,7 +742,7 @@ void f1_impl(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, St
   f1.lgnt = g.lgW - sh.lgS;
   f1.bufE = col_bufE(sh);
   f1.nitems = (1 << f1.lgnt) * nsets;
-  launch_op<R>(f1, col_threads(sh), 1, stop, s);
+  launch_op<R>(f1, col_threads(sh), 0, stop, s);
 }
 
 template <typename R>
