@@ -119,7 +119,7 @@ def pvb_loss(z_in, z_out, z_t):
 
 def _socs_gradient_dev(mask, z, z_t, kernels, sigma_z, dose):
     m = _f64(mask)
-    dks = kernels.device(m.shape)
+    dks = litho.device_kernels(kernels, m.shape)
     zz, zt = _bcast_pair(z, z_t)
     out = nv.empty(m.shape, np.float64)
     md, zd, ztd = nv.to_dev(m), nv.to_dev(zz), nv.to_dev(zt)
@@ -257,8 +257,8 @@ def _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation):
             raise ValueError(f"kernel set condition {ks.condition!r} does not match "
                              f"process condition {sel!r}")
     prec = cfg.precision
-    fk = focus_kernels.device(shape, prec)
-    dk = defocus_kernels.device(shape, prec)
+    fk = litho.device_kernels(focus_kernels, shape, prec)
+    dk = litho.device_kernels(defocus_kernels, shape, prec)
     return target, m, fk, dk
 
 

@@ -404,3 +404,19 @@ def test_modulation_search_small():
     losses = [l for _, l in r.candidates]
     assert max(losses) - min(losses) <= 1e-9 * max(losses)
     assert r.best_delta_h == 0.0
+
+
+@pytest.mark.gpu
+def test_reference_kernelset_objects_accepted():
+    """Function-level drop-in: objects with the reference
+    KernelSet fields (kernels[i].coeffs / .weight, condition) are accepted and
+    give results identical to the package's own KernelSet."""
+    from types import SimpleNamespace
+    nv.set_precision("fp64")
+    f, d, F, D = kernels(9, 2, 0)
+    ref_like = SimpleNamespace(kernels=[SimpleNamespace(coeffs=c, weight=float(w)) for c, w in zip(*f)],
+                               condition="focus")
+    m = (np.random.default_rng(5).random((64, 64)) < 0.3).astype(np.float64)
+    a = b2.aerial_intensity(m, F, b2.NOMINAL)
+    b = b2.aerial_intensity(m, ref_like, b2.NOMINAL)
+    assert np.array_equal(a, b)
