@@ -143,6 +143,8 @@ def to_dev(a, dtype=np.float64):
     """Host array -> contiguous device tensor (copy)."""
     t = torch()
     arr = np.ascontiguousarray(np.asarray(a, dtype=dtype))
+    if not arr.flags.writeable:
+        arr = arr.copy()
     return t.from_numpy(arr).to("cuda", non_blocking=False)
 
 
