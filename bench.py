@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-solve", action="store_true")
+    p.add_argument("--clips", type=int, default=64, help="config 3 batch size (0 = skip)")
     return p.parse_args()
 
 
@@ -196,7 +197,7 @@ def b200_arm(args, world, rank, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2303_12529_b200 as b2
     from paper_2303_12529_b200 import _native as nv
-    from paper_2303_12529_b200 import inputs
+    from paper_2303_12529_b200 import inputs, parallel
 
     nv.set_precision(args.precision)
     K, W = args.steps, args.warmup
@@ -237,11 +238,7 @@ def b200_arm(args, world, rank, local):
     ms = ev0.elapsed_time(ev1)
     nv.check(L.lsopc_session_poll(sess, ctypes.byref(stopped), None))
     assert not stopped.value, "stop rule fired inside the timed region"
-    ms_max = ms
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = parallel.max_over_ranks(ms, device="cuda")
     value = world * K / (ms_max / 1e3)
 
     # ---- per-pass CUDA-event timing on the session stream (after the timed region)
@@ -269,34 +266,47 @@ def b200_arm(args, world, rank, local):
             traffic = None
 
     # ---- e2e through the public API: host target in, host mask/phi out -------
-    torch.cuda.synchronize()
+    # b2.optimize(host uint8 target) with K iterations: H2D of the target,
+    # TSDF, K iterations, final hard prints, D2H of best phi + final mask, and
+    # the host shot count, all inside the timed call.  One warm-up call, then
+    # the median of 3 (max over ranks).
     cfg_e2e = b2.OptConfig(max_iters=K, stop_patience=10**9, precision=args.precision)
-    t0 = time.perf_counter()
-    r = b2.optimize(clip, focus, defocus, cfg_e2e)
-    torch.cuda.synchronize()
-    t_e2e = time.perf_counter() - t0
-    assert r.iters_run == K
-    e2e_val = K / t_e2e
-    if world > 1:
-        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_val = world * K / float(t.item())
+    b2.optimize(clip, focus, defocus, cfg_e2e)
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = b2.optimize(clip, focus, defocus, cfg_e2e)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        assert r.iters_run == K
+    t_e2e = parallel.max_over_ranks(statistics.median(times), device="cuda")
+    e2e_val = world * K / t_e2e
 
-    # ---- full default solve of this rank's clip (clips/s) --------------------
-    solve = None
+    # ---- config 2: full default solve of this rank's clip (latency) ----------
+    solve = batch = None
     if not args.no_solve:
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         rs = b2.optimize(clip, focus, defocus, b2.OptConfig(precision=args.precision))
         torch.cuda.synchronize()
-        t_solve = time.perf_counter() - t0
-        lat = t_solve
-        if world > 1:
-            t = torch.tensor([t_solve], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            lat = float(t.item())
+        lat = parallel.max_over_ranks(time.perf_counter() - t0, device="cuda")
         solve = {"iters": rs.iters_run, "latency_s": round(lat, 4), "wall_time_s": round(rs.wall_time, 4),
-                 "clips_per_s": round(world / lat, 3), "l2": rs.metrics.l2, "pvband": rs.metrics.pvband,
-                 "shots": rs.metrics.shots}
+                 "l2": rs.metrics.l2, "pvband": rs.metrics.pvband, "shots": rs.metrics.shots,
+                 "note": "b2.optimize(iccad_like_clip(rank), OptConfig()) to the reference's stop rule; "
+                         "incl. TSDF, final prints, shot count"}
+        # ---- config 3: a batch of clips sharded clip-parallel, no collective ---
+        if args.clips > 0:
+            clips = parallel.LazyClips(args.clips, seed0=0)
+            recs, secs = parallel.optimize_batch(clips, focus, defocus, b2.OptConfig(precision=args.precision),
+                                                 synchronize=torch.cuda.synchronize)
+            batch = {"clips": args.clips, "seconds": round(secs, 3), "clips_per_s": round(args.clips / secs, 3),
+                     "iters_total": int(sum(x.iters for x in recs)),
+                     "iters_per_s": round(sum(x.iters for x in recs) / secs, 2),
+                     "mean_l2": round(float(np.mean([x.l2 for x in recs])), 1),
+                     "mean_pvband": round(float(np.mean([x.pvband for x in recs])), 1),
+                     "note": f"iccad_like_clip(0..{args.clips - 1}) round-robin over {world} GPU(s), "
+                             "default OptConfig, each clip solved to the stop rule"}
 
     if rank != 0:
         if world > 1:
@@ -322,8 +332,8 @@ def b200_arm(args, world, rank, local):
                    "l2_flush": "not needed: per-iteration working set (spectra 768 MiB+) > 126 MB L2"},
         "e2e": {"value": round(e2e_val, 3), "unit": "iters/s",
                 "h2d_bytes_per_step": round(n / K), "d2h_bytes_per_step": round(9 * n / K),
-                "note": f"b2.optimize(host target, max_iters={K}) incl. TSDF, final prints, shot count; "
-                        f"{t_e2e:.3f} s"},
+                "note": f"b2.optimize(host uint8 target, max_iters={K}): H2D target, TSDF, {K} iterations, "
+                        f"final prints, D2H best phi + mask, host shot count; median of 3 = {t_e2e:.3f} s"},
         "roofline": {"bound": "hbm", "achieved": round(per_pass[dom]["gbs"], 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(per_pass[dom]["frac"], 4), "traffic": traffic,
                      "kernel": per_pass[dom]["name"], "peak_source": src,
@@ -341,6 +351,7 @@ def b200_arm(args, world, rank, local):
         "gpu_launches": launches_per_iter * K,
         "clocks": clk.summary(),
         "solve": solve,
+        "batch": batch,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

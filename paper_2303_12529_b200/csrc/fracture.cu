@@ -11,6 +11,7 @@
 // reference's strict comparison returns exactly the reference's pick.
 #include "../../include/lsopc_b200.h"
 
+#include <cstdint>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -27,16 +28,19 @@ inline bool better(const Cand& c, const Cand& best) {
   return c.area > best.area || (c.area == best.area && (c.y < best.y || (c.y == best.y && c.x < best.x)));
 }
 
-// histogram-stack sweep of one bottom row (metrics.py:67-86)
-Cand sweep_row(const int* heights, int W, int y, std::vector<int>& stack) {
-  Cand best;
+// histogram-stack sweep of columns [a, b) of one bottom row, all heights > 0
+// inside (metrics.py:67-86 restricted to one run: no rectangle crosses a
+// zero-height column, and within a row two candidates with equal
+// (area, top, left) are the same rectangle, so sweeping runs separately and
+// keeping the strict `better` order returns the reference's pick)
+void sweep_run(const int* heights, int a, int b, int y, int* stack, Cand& best) {
   int top = -1;
-  for (int x = 0; x <= W; ++x) {
-    const int cur = x < W ? heights[x] : 0;
+  for (int x = a; x <= b; ++x) {
+    const int cur = x < b ? heights[x] : 0;
     while (top >= 0 && heights[stack[top]] > cur) {
       const int hh = heights[stack[top]];
       --top;
-      const int left = top >= 0 ? stack[top] + 1 : 0;
+      const int left = top >= 0 ? stack[top] + 1 : a;
       Cand c;
       c.area = (long long)hh * (x - left);
       c.x = left;
@@ -46,6 +50,27 @@ Cand sweep_row(const int* heights, int W, int y, std::vector<int>& stack) {
       if (better(c, best)) best = c;
     }
     stack[++top] = x;
+  }
+}
+
+// sweep of one bottom row: heights > 0 exactly where the row's mask byte is 1;
+// zero runs are skipped 8 bytes at a time
+Cand sweep_row(const int* heights, const uint8_t* mrow, int W, int y, std::vector<int>& stack) {
+  Cand best;
+  int x = 0;
+  while (x < W) {
+    while (x + 8 <= W) {
+      uint64_t w8;
+      std::memcpy(&w8, mrow + x, 8);
+      if (w8) break;
+      x += 8;
+    }
+    while (x < W && !mrow[x]) ++x;
+    if (x >= W) break;
+    int b = x;
+    while (b < W && mrow[b]) ++b;
+    sweep_run(heights, x, b, y, stack.data(), best);
+    x = b;
   }
   return best;
 }
@@ -65,7 +90,7 @@ extern "C" int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* r
     }
   std::vector<int> stack(W + 1);
   std::vector<Cand> rowbest(H);
-  for (int y = 0; y < H; ++y) rowbest[y] = sweep_row(&hts[(size_t)y * W], W, y, stack);
+  for (int y = 0; y < H; ++y) rowbest[y] = sweep_row(&hts[(size_t)y * W], &m[(size_t)y * W], W, y, stack);
   size_t k = 0;
   while (true) {
     Cand best;
@@ -91,7 +116,7 @@ extern "C" int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* r
         if (y > ymax) ymax = y;
       }
     }
-    for (int y = best.y; y <= ymax; ++y) rowbest[y] = sweep_row(&hts[(size_t)y * W], W, y, stack);
+    for (int y = best.y; y <= ymax; ++y) rowbest[y] = sweep_row(&hts[(size_t)y * W], &m[(size_t)y * W], W, y, stack);
   }
   *count = k;
   return LSOPC_OK;

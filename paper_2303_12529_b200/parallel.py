@@ -1,0 +1,112 @@
+"""Clip-parallel execution across GPUs (BASELINE configs[2]).
+
+Independent clips are the unit of work: clip i runs on rank i mod world
+(round robin), each rank owns its own device spectra, and no collective
+touches the data path.  The only communication is the gather of the small
+per-clip records at the end and the max-over-ranks of the timings, over
+whatever `torch.distributed` backend the caller initialised (NCCL on the GPU
+box, gloo in the CPU tests).
+
+The reference has no multi-process code; its contract allows independent runs
+to execute concurrently (`SPEC.md:432`), which is what this module does.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import asdict, dataclass
+
+
+@dataclass
+class ClipRecord:
+    """Per-clip outcome of one solve (the fields of `MetricsReport`, metrics.py:16-31)."""
+    index: int
+    rank: int
+    l2: int
+    pvband: int
+    shots: int
+    iters: int
+    wall_time: float
+
+
+def world_info(group=None):
+    """(rank, world size) of the default group, or (0, 1) without one."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def shard(n_items, rank, world):
+    """Indices owned by `rank`: round robin, disjoint, covering 0..n_items-1."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world size {world}")
+    return list(range(rank, n_items, world))
+
+
+def max_over_ranks(value, group=None, device=None):
+    """Max of a float over all ranks (identity without a process group)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def gather_records(records, group=None):
+    """All ranks' records, ordered by clip index (every rank gets the list)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return sorted(records, key=lambda r: r.index)
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, [asdict(r) for r in records], group=group)
+    merged = [ClipRecord(**d) for part in out for d in part]
+    return sorted(merged, key=lambda r: r.index)
+
+
+def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, solver=None,
+                   synchronize=None):
+    """Solve every clip of `targets` (a sequence of 2-D uint8 layouts; a
+    `LazyClips` lets each rank generate only its own clips) on the rank that
+    owns it.  Returns (records of all clips ordered by index,
+    seconds = max over ranks of this rank's solve time).
+
+    `solver(target, focus, defocus, cfg) -> OptimizationResult` defaults to
+    `optimizer.optimize` (the device loop); tests inject a stub.
+    """
+    if solver is None:
+        from .optimizer import optimize as solver
+    rank, world = world_info(group)
+    mine = [(i, targets[i]) for i in shard(len(targets), rank, world)]  # inputs built before timing
+    if synchronize:
+        synchronize()
+    t0 = time.perf_counter()
+    records = []
+    for i, target in mine:
+        r = solver(target, focus_kernels, defocus_kernels, cfg)
+        m = r.metrics
+        records.append(ClipRecord(i, rank, int(m.l2), int(m.pvband), int(m.shots), int(r.iters_run),
+                                  float(r.wall_time)))
+    if synchronize:
+        synchronize()
+    seconds = max_over_ranks(time.perf_counter() - t0, group)
+    return gather_records(records, group), seconds
+
+
+class LazyClips:
+    """Sequence of synthetic clips generated on demand (each rank builds only
+    the clips it owns): clip i = `iccad_like_clip(seed=seed0 + i)`."""
+
+    def __init__(self, n, seed0=0, side=2048):
+        self.n, self.seed0, self.side = n, seed0, side
+
+    def __len__(self):
+        return self.n
+
+    def __getitem__(self, i):
+        from .inputs import iccad_like_clip
+        if not 0 <= i < self.n:
+            raise IndexError(i)
+        return iccad_like_clip(seed=self.seed0 + i, n=self.side)
