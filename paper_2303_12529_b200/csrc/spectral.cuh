@@ -46,7 +46,8 @@ constexpr int kMaxK = 64;  // kernels per set carried in a launch
 // B200: whole-tile column items stream at 6.2 TB/s; a 4-row item reads 128 B
 // chunks of a 4-wide tiling at 73% of that and 256 B chunks of an 8-wide
 // tiling at full speed, while a 4-column item of an 8-wide tiling runs at 91%).
-constexpr int kLgTile = 2;   // U_k, V, M^, spectra: column items read whole tiles
+// U_k, V, M^, spectra: 32 B tile rows, so a column item (4 x c64 or 2 x c128) is a whole tile
+template <typename C> constexpr int lg_tile() { return sizeof(C) == 8 ? 2 : 1; }
 constexpr int kLgTileT = 3;  // T_k: read by the F2 row pass as 256 B chunks
 
 template <typename R> struct Shape {
@@ -60,7 +61,7 @@ template <typename R> struct Shape {
   LS_HD Lay ct() const { return Lay{H, lgT}; }   // column-tiled layout of spectral fields
   LS_HD Lay rm() const { return Lay{H, lgW}; }   // row-major
   // compile-time-geometry path allowed (layout tile width is the constant one)
-  LS_HD bool fast() const { return lgT == kLgTile && lgTT == kLgTileT; }
+  LS_HD bool fast() const { return lgT == lg_tile<typename CT<R>::C>() && lgTT == kLgTileT; }
   LS_HD Lay ctT() const { return Lay{H, lgTT}; }  // layout of the T_k fields
 };
 
@@ -71,7 +72,7 @@ template <typename R> Shape<R> shape_of(const Grid& g) {
   s.H = g.H; s.W = g.W; s.lgH = g.lgH; s.lgW = g.lgW;
   s.lgS = std::max(0, std::min(g.lgW, ilog2i(E) - g.lgH));
   s.lgR = std::max(0, std::min(g.lgH, ilog2i(E) - g.lgW));
-  s.lgT = std::min(g.lgW, kLgTile);
+  s.lgT = std::min(g.lgW, lg_tile<typename CT<R>::C>());
   s.lgTT = std::min(g.lgW, kLgTileT);
   s.twsH = g.lgnmax - g.lgH;
   s.twsW = g.lgnmax - g.lgW;
@@ -160,7 +161,7 @@ template <int LGN, int STRIDE> LS_D int nat_row(int seq, int j, int r, int lgn) 
   else return (seq << lgn) + j;
 }
 // column-tiled element (y = j + r*STRIDE, x); fast path has tile width 2^kLgTile
-template <int LGN, int STRIDE, int LGT = kLgTile> LS_D size_t ct_col(const Lay& L, int j, int r, int x) {
+template <int LGN, int STRIDE, typename C, int LGT = lg_tile<C>()> LS_D size_t ct_col(const Lay& L, int j, int r, int x) {
   if constexpr (LGN > 0) {
     constexpr int T = 1 << LGT;
     return (((size_t)(x >> LGT) * L.H + j) << LGT) + (x & (T - 1)) + (size_t)r * (STRIDE << LGT);
@@ -169,7 +170,7 @@ template <int LGN, int STRIDE, int LGT = kLgTile> LS_D size_t ct_col(const Lay& 
   }
 }
 // column-tiled element (y, x = j + r*STRIDE)
-template <int LGN, int STRIDE, int LGT = kLgTile> LS_D size_t ct_row(const Lay& L, int y, int j, int r) {
+template <int LGN, int STRIDE, typename C, int LGT = lg_tile<C>()> LS_D size_t ct_row(const Lay& L, int y, int j, int r) {
   if constexpr (LGN > 0) {
     constexpr int T = 1 << LGT;
     static_assert(STRIDE % T == 0, "row stride must be a multiple of the tile width");
@@ -216,7 +217,7 @@ template <typename R> struct MaskRowsOp : OpBase {
       }
       return cmk(m, (R)0);
     }
-    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_row<LGN, ST>(L, y0 + seq, j, r)] = v; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_row<LGN, ST, C>(L, y0 + seq, j, r)] = v; }
   };
   template <class St> LS_D void step(St&, int it, int, C* b, C*) const {
     const Geo g = sh.grow();
@@ -252,12 +253,12 @@ template <typename R, typename RO, bool INV> struct ColsOp : OpBase {
     R scale;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)] * scale; }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
-      out[ct_col<LGN, ST>(L, j, r, x0 + seq)] = cmk((RO)v.x, (RO)v.y);
+      out[ct_col<LGN, ST, C>(L, j, r, x0 + seq)] = cmk((RO)v.x, (RO)v.y);
     }
   };
   template <class St> LS_D void step(St&, int it, int, C* b, C*) const {
     const Geo g = sh.gcol();
-    eng::dispatch<C>(g, sh.fast() && Lout.lgw == kLgTile, [&](auto fx) {
+    eng::dispatch<C>(g, sh.fast() && Lout.lgw == lg_tile<C>(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       F<LGN> f{b, out, Lout, it << sh.lgS, sh.lgS, scale};
       eng::run_fix<LGN, true, INV>(g, b, tw, f);
@@ -334,7 +335,7 @@ template <typename R> struct F1Op : OpBase {
     Lay L;
     int x0;
     template <int ST> LS_D void operator()(int seq, int j, int r, int slot) const {
-      S.mh[slot] = __ldg(&mhat[ct_col<LGN, ST>(L, j, r, x0 + seq)]);
+      S.mh[slot] = __ldg(&mhat[ct_col<LGN, ST, C>(L, j, r, x0 + seq)]);
     }
   };
   LS_D void begin(State& S, int it, C*) const {
@@ -358,7 +359,7 @@ template <typename R> struct F1Op : OpBase {
       else return cmul(mhat[Lm.at(j, x0 + seq)], x) * scale;
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
-      out[ct_col<LGN, ST, kLgTileT>(L, j, r, x0 + seq)] = v;
+      out[ct_col<LGN, ST, C, kLgTileT>(L, j, r, x0 + seq)] = v;
     }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
@@ -474,7 +475,7 @@ template <typename R> struct A1Op : OpBase {
       if constexpr (LGN > 0) return x * S.g[slot];
       else return x * gate[(size_t)(y0 + seq) * W + j];
     }
-    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_row<LGN, ST>(L, y0 + seq, j, r)] = v; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_row<LGN, ST, C>(L, y0 + seq, j, r)] = v; }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
     const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
@@ -512,7 +513,7 @@ template <typename R> struct A2Op : OpBase {
     Lay L;
     int x0;
     template <int ST> LS_D void operator()(int seq, int j, int r, int slot) const {
-      h[slot] = __ldg(&spec[ct_col<LGN, ST>(L, j, r, x0 + seq)]);
+      h[slot] = __ldg(&spec[ct_col<LGN, ST, C>(L, j, r, x0 + seq)]);
     }
   };
   template <int LGN> struct F {
@@ -549,7 +550,7 @@ template <typename R> struct A2Op : OpBase {
     Lay L;
     int x0, lgS;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)]; }
-    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_col<LGN, ST>(L, j, r, x0 + seq)] = v; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_col<LGN, ST, C>(L, j, r, x0 + seq)] = v; }
   };
   LS_D void end(State& S, int it, C* b, C*) const {
     const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
@@ -591,7 +592,7 @@ template <typename R> struct A3Op : OpBase {
     int y0, lgn, W;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const C x = b[nat_row<LGN, ST>(seq, j, r, lgn)];
-      return v1 ? x + __ldg(&v1[ct_row<LGN, ST>(L, y0 + seq, j, r)]) : x;
+      return v1 ? x + __ldg(&v1[ct_row<LGN, ST, C>(L, y0 + seq, j, r)]) : x;
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
       const size_t p = rm_row<LGN, ST>(W, y0 + seq, j, r);

@@ -415,7 +415,7 @@ def test_reference_kernelset_objects_accepted():
     nv.set_precision("fp64")
     f, d, F, D = kernels(9, 2, 0)
     ref_like = SimpleNamespace(kernels=[SimpleNamespace(coeffs=c, weight=float(w)) for c, w in zip(*f)],
-                               condition="focus")
+                               condition="focus", side=9)  # litho.py:46-69 fields
     m = (np.random.default_rng(5).random((64, 64)) < 0.3).astype(np.float64)
     a = b2.aerial_intensity(m, F, b2.NOMINAL)
     b = b2.aerial_intensity(m, ref_like, b2.NOMINAL)
