@@ -158,6 +158,20 @@ def to_host(t):
     return t.cpu().numpy()
 
 
+_pinned = {}
+
+
+def pinned_like(t):
+    """A cached page-locked host tensor with t's shape and dtype (staging for
+    fast device-to-host copies; callers copy out of it before reuse)."""
+    key = (tuple(t.shape), t.dtype)
+    buf = _pinned.get(key)
+    if buf is None:
+        buf = torch().empty(t.shape, dtype=t.dtype, pin_memory=True)
+        _pinned[key] = buf
+    return buf
+
+
 # ---------------------------------------------------------------------------
 # precision tiers
 

@@ -14,6 +14,7 @@ struct DevState {
   double beta;
   double vmax, gmax, dt;
   int stopped, improved, use_beta, streak, nhist, nonfinite_it;
+  int it;  // index of the iteration in flight (advanced by the update's control kernel)
 };
 
 struct LoopCfg {
@@ -35,9 +36,9 @@ void launch_ls_velocity(int H, int W, const double* phi, const double* v, const 
 void launch_ls_update(size_t n, double* phi, const double* u, const double* gm, double lo, double hi,
                       const DevState* st, uint8_t* mask, double* partials, cudaStream_t s);
 void launch_copy_best(size_t n, const double* phi, double* best, const DevState* st, cudaStream_t s);
-void launch_after_forward(const double* part, int nb, LoopCfg c, int it, DevState* st, double* hist,
-                          cudaStream_t s);
-void launch_after_grad(const double* dots, int nb, int restart, DevState* st, cudaStream_t s);
+void launch_after_forward(const double* part, int nb, LoopCfg c, DevState* st, double* hist, cudaStream_t s);
+// restart_every: Polak-Ribiere restart period (optimizer.py:253); iteration 0 always restarts
+void launch_after_grad(const double* dots, int nb, int restart_every, DevState* st, cudaStream_t s);
 void launch_after_velocity(const double* part, int nb, double eta, DevState* st, double* hist, cudaStream_t s);
 void launch_after_update(const double* part, int nb, DevState* st, double* hist, cudaStream_t s);
 void launch_elementwise(int op, size_t n, const double* a, const double* b, double p0, double p1, double p2,

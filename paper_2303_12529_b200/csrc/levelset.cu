@@ -206,7 +206,7 @@ LS_D void reduce_partials(const double* part, int nb, double (&out)[NV], double*
 }
 
 // optimizer.py:238-251: loss, best iterate, patience
-__global__ void k_after_forward(const double* part, int nb, LoopCfg c, int it, DevState* st, double* hist) {
+__global__ void k_after_forward(const double* part, int nb, LoopCfg c, DevState* st, double* hist) {
   __shared__ double red[64];
   if (st->stopped) return;
   double l[2];
@@ -219,7 +219,7 @@ __global__ void k_after_forward(const double* part, int nb, LoopCfg c, int it, D
   st->l_dso = l_dso;
   st->improved = 0;
   if (!isfinite(l_dso)) {
-    st->nonfinite_it = it;
+    st->nonfinite_it = st->it;
     st->stopped = 1;
     return;
   }
@@ -241,9 +241,10 @@ __global__ void k_after_forward(const double* part, int nb, LoopCfg c, int it, D
 }
 
 // optimizer.py:154-169,253: Polak-Ribiere beta with restart
-__global__ void k_after_grad(const double* dots, int nb, int restart, DevState* st) {
+__global__ void k_after_grad(const double* dots, int nb, int restart_every, DevState* st) {
   __shared__ double red[64];
   if (st->stopped) return;
+  const int restart = st->it == 0 || st->it % restart_every == 0;
   double s[2] = {0.0, 0.0};
   if (!restart) reduce_partials<2, false>(dots, nb, s, red);
   if (threadIdx.x != 0) return;
@@ -286,6 +287,7 @@ __global__ void k_after_update(const double* part, int nb, DevState* st, double*
   h[0] = st->l_ilt; h[1] = st->l_pvb; h[2] = st->l_dso; h[3] = st->dt; h[4] = st->vmax; h[5] = m[0];
   h[6] = st->gmax;
   st->nhist += 1;
+  st->it += 1;
 }
 
 // ---- elementwise API operators -------------------------------------------------
@@ -324,7 +326,7 @@ k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restric
       case RD_DOT: acc[0] += a[i] * b[i]; break;
       case RD_DOTDIFF: acc[0] += a[i] * (a[i] - b[i]); break;
       case RD_MAXABS: acc[0] = fmax(acc[0], fabs(a[i])); break;
-      case RD_COUNTNEQ8: acc[0] += (a8[i] != b8[i]) ? 1.0 : 0.0; break;
+      case RD_COUNTNEQ8: acc[0] += (a8[i] != (b8 ? b8[i] : 0)) ? 1.0 : 0.0; break;  // b8 null: vs 0
       case RD_COUNTNEQ: acc[0] += (a[i] != b[i]) ? 1.0 : 0.0; break;
       case RD_NONFINITE: if (!isfinite(a[i])) acc[0] = fmax(acc[0], (double)(n - i)); break;
       default: break;
@@ -367,12 +369,11 @@ void launch_ls_update(size_t n, double* phi, const double* u, const double* gm, 
 void launch_copy_best(size_t n, const double* phi, double* best, const DevState* st, cudaStream_t s) {
   k_copy_best<<<kBlocks, kThreads, 0, s>>>(n, phi, best, st);
 }
-void launch_after_forward(const double* part, int nb, LoopCfg c, int it, DevState* st, double* hist,
-                          cudaStream_t s) {
-  k_after_forward<<<1, 256, 0, s>>>(part, nb, c, it, st, hist);
+void launch_after_forward(const double* part, int nb, LoopCfg c, DevState* st, double* hist, cudaStream_t s) {
+  k_after_forward<<<1, 256, 0, s>>>(part, nb, c, st, hist);
 }
-void launch_after_grad(const double* dots, int nb, int restart, DevState* st, cudaStream_t s) {
-  k_after_grad<<<1, 256, 0, s>>>(dots, nb, restart, st);
+void launch_after_grad(const double* dots, int nb, int restart_every, DevState* st, cudaStream_t s) {
+  k_after_grad<<<1, 256, 0, s>>>(dots, nb, restart_every, st);
 }
 void launch_after_velocity(const double* part, int nb, double eta, DevState* st, double* hist, cudaStream_t s) {
   k_after_velocity<<<1, 256, 0, s>>>(part, nb, eta, st, hist);

@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -70,6 +71,10 @@ struct DevBuf {
 
 struct lsopc_plan {
   Grid g{};
+  // idle sessions kept for reuse by the next lsopc_session_create with the
+  // same kernel sets and config: their buffers and captured graphs survive
+  // (cudaMalloc/cudaFree and graph instantiation cost more than a 2048^2 solve)
+  std::vector<lsopc_session*> pool;
   // T: per-kernel work fields (T_k / U_k) of the spectral passes, grown to the
   // largest (focus + defocus) kernel count used on this plan.
   // A: per-kernel row-major fields A_k (F2 -> A1).
@@ -85,6 +90,8 @@ struct lsopc_plan {
     A.ensure((size_t)nk_total * n() * g.csize());
   }
 };
+
+void lsb_purge_pool(lsopc_plan* p, const lsopc_kset* ks);
 
 struct lsopc_kset {
   lsopc_plan* plan = nullptr;
@@ -217,6 +224,7 @@ int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
 int lsopc_plan_destroy(lsopc_plan* plan) {
   return guarded([&] {
     cudaDeviceSynchronize();
+    if (plan) lsb_purge_pool(plan, nullptr);
     delete plan;
   });
 }
@@ -269,6 +277,7 @@ int lsopc_kset_download(const lsopc_kset* ks, double* out, void* stream) {
 int lsopc_kset_destroy(lsopc_kset* ks) {
   return guarded([&] {
     cudaDeviceSynchronize();
+    if (ks && ks->plan) lsb_purge_pool(ks->plan, ks);
     delete ks;
   });
 }
@@ -368,11 +377,7 @@ int lsopc_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_lower
       throw Error(LSOPC_EINVAL, "truncation bounds must satisfy D_l < 0 < D_u");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t n = (size_t)H * W;
-    DevBuf ones;
-    ones.ensure(n);
-    ck(cudaMemsetAsync(ones.p, 0, n, s), "memset");
-    double diff = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, mask, ones.as<uint8_t>(), nullptr, s);
-    ones.release();
+    double diff = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, mask, nullptr, nullptr, s);
     if (diff == 0.0 || diff == (double)n) throw Error(LSOPC_EDEGENERATE, "mask is uniform: no boundary exists");
     DevBuf si, sf;
     si.ensure(tsdf_scratch_i32(H, W) * sizeof(int));
@@ -417,9 +422,18 @@ struct lsopc_session {
   lsopc_config cfg{};
   cudaStream_t s = nullptr;
   DevBuf target, phi, best, v[2], d[2], u, mask, mod, hist, state, part_ls, part_up, dots, gm;
-  int it = 0;
+  int it = 0;  // iterations enqueued
   bool have_mod = false;
+  // one DSO iteration captured as a CUDA graph per buffer parity (it & 1)
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  int* hflag = nullptr;  // pinned host copies of DevState::stopped (async polling)
+  cudaEvent_t ev[2] = {nullptr, nullptr};
   ~lsopc_session() {
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (hflag) cudaFreeHost(hflag);
     for (DevBuf* b : {&target, &phi, &best, &v[0], &v[1], &d[0], &d[1], &u, &mask, &mod, &hist, &state, &part_ls,
                       &part_up, &dots, &gm})
       b->release();
@@ -429,14 +443,64 @@ struct lsopc_session {
 
 namespace {
 
+constexpr size_t kPoolCap = 4;
+
+bool same_key(const lsopc_session* ss, const lsopc_kset* f, const lsopc_kset* d, const lsopc_config& c,
+              bool have_mod) {
+  return ss->focus == f && ss->defocus == d && ss->have_mod == have_mod &&
+         std::memcmp(&ss->cfg, &c, sizeof(c)) == 0;
+}
+
+lsopc_session* take_pooled(lsopc_plan* p, const lsopc_kset* f, const lsopc_kset* d, const lsopc_config& c,
+                           bool have_mod) {
+  for (size_t i = 0; i < p->pool.size(); ++i) {
+    if (same_key(p->pool[i], f, d, c, have_mod)) {
+      lsopc_session* ss = p->pool[i];
+      p->pool.erase(p->pool.begin() + i);
+      return ss;
+    }
+  }
+  return nullptr;
+}
+
+void give_to_pool(lsopc_session* ss) {
+  lsopc_plan* p = ss->plan;
+  p->pool.insert(p->pool.begin(), ss);
+  while (p->pool.size() > kPoolCap) {
+    delete p->pool.back();
+    p->pool.pop_back();
+  }
+}
+
+// drop pooled sessions that reference a kernel set (before it is freed), or all
+void purge_pool(lsopc_plan* p, const lsopc_kset* ks) {
+  for (size_t i = 0; i < p->pool.size();) {
+    if (!ks || p->pool[i]->focus == ks || p->pool[i]->defocus == ks) {
+      delete p->pool[i];
+      p->pool.erase(p->pool.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+}
+
+}  // namespace
+
+void lsb_purge_pool(lsopc_plan* p, const lsopc_kset* ks) { purge_pool(p, ks); }
+
+namespace {
+
 // Pass boundaries inside one iteration, for per-pass CUDA-event timing.
 enum { PS_MASK = 0, PS_F1, PS_F2, PS_RESIST, PS_A1, PS_A2, PS_A3, PS_LS, PS_N };
 
-void enqueue_iteration(lsopc_session* ss, int it, cudaEvent_t* ev = nullptr) {
+// One iteration on buffers of parity `par`; every iteration-dependent
+// decision (restart, record index, stop) reads the device state, so the same
+// launch sequence serves every iteration of that parity (graph capture).
+void enqueue_iteration(lsopc_session* ss, int par, cudaStream_t s, cudaEvent_t* ev = nullptr) {
   lsopc_plan* p = ss->plan;
   const Grid& g = p->g;
   const size_t n = g.n();
-  cudaStream_t s = ss->s;
+  const int it = par;
   DevState* st = ss->st();
   StopFlag stop = &st->stopped;
   const lsopc_config& c = ss->cfg;
@@ -461,7 +525,7 @@ void enqueue_iteration(lsopc_session* ss, int it, cudaEvent_t* ev = nullptr) {
   launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr, nullptr,
                 nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s);
   LoopCfg lc{c.alpha, c.beta, c.stop_rel_tol, c.stop_patience};
-  launch_after_forward(p->partials.as<double>(), reduce_blocks(), lc, it, st, ss->hist.as<double>(), s);
+  launch_after_forward(p->partials.as<double>(), reduce_blocks(), lc, st, ss->hist.as<double>(), s);
   launch_copy_best(n, ss->phi.as<double>(), ss->best.as<double>(), st, s);
   mark(4);
   // adjoint: U_k, then one frequency-domain accumulator per set and one inverse
@@ -469,11 +533,10 @@ void enqueue_iteration(lsopc_session* ss, int it, cudaEvent_t* ev = nullptr) {
   mark(5);
   launch_a2(g, sets, 2, stop, s);
   mark(6);
-  int ndots = launch_adjoint_finish(g, p->V0.p, p->V1.p, 4.0 * c.sigma_z / (double)n, v, it > 0 ? vprev : nullptr,
+  int ndots = launch_adjoint_finish(g, p->V0.p, p->V1.p, 4.0 * c.sigma_z / (double)n, v, vprev,
                                     ss->dots.as<double>(), stop, s);
   mark(7);
-  const int restart = (it % c.cg_restart_every == 0) ? 1 : 0;
-  launch_after_grad(ss->dots.as<double>(), ndots, restart || it == 0, st, s);
+  launch_after_grad(ss->dots.as<double>(), ndots, c.cg_restart_every, st, s);
   // level-set step
   launch_ls_velocity(g.H, g.W, ss->phi.as<double>(), v, dprev, ss->have_mod ? ss->mod.as<double>() : nullptr,
                      c.curvature_weight, c.use_curvature, st, d, ss->u.as<double>(),
@@ -504,38 +567,40 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Grid& g = plan->g;
     const size_t n = g.n();
-    auto* ss = new lsopc_session();
+    lsopc_session* ss = take_pooled(plan, focus, defocus, *cfg, mod_dev != nullptr);
+    const bool fresh = ss == nullptr;
+    if (fresh) ss = new lsopc_session();
     try {
       ss->plan = plan;
       ss->focus = focus;
       ss->defocus = defocus;
       ss->cfg = *cfg;
       ss->s = s;
-      ss->target.ensure(n);
-      ck(cudaMemcpyAsync(ss->target.p, target_dev, n, cudaMemcpyDeviceToDevice, s), "memcpy");
-      ss->phi.ensure(n * 8);
-      ss->best.ensure(n * 8);
-      for (int i = 0; i < 2; ++i) {
-        ss->v[i].ensure(n * 8);
-        ss->d[i].ensure(n * 8);
+      ss->it = 0;
+      ss->have_mod = mod_dev != nullptr;
+      if (fresh) {
+        ss->target.ensure(n);
+        ss->phi.ensure(n * 8);
+        ss->best.ensure(n * 8);
+        for (int i = 0; i < 2; ++i) {
+          ss->v[i].ensure(n * 8);
+          ss->d[i].ensure(n * 8);
+        }
+        ss->u.ensure(n * 8);
+        if (cfg->update_form) ss->gm.ensure(n * 8);
+        ss->mask.ensure(n);
+        ss->hist.ensure((size_t)(cfg->max_iters + 1) * 7 * sizeof(double));
+        ss->state.ensure(sizeof(DevState));
+        ss->part_ls.ensure((size_t)ls_blocks() * 2 * sizeof(double));
+        ss->part_up.ensure((size_t)ls_blocks() * sizeof(double));
+        ss->dots.ensure((size_t)(finish_max_blocks() + 1) * 2 * sizeof(double));
+        if (mod_dev) ss->mod.ensure(n * 8);
+        plan->ensure_T(focus->nk + defocus->nk);
       }
-      ss->u.ensure(n * 8);
-      if (cfg->update_form) ss->gm.ensure(n * 8);
-      ss->mask.ensure(n);
-      ss->hist.ensure((size_t)(cfg->max_iters + 1) * 7 * sizeof(double));
-      ss->state.ensure(sizeof(DevState));
-      ss->part_ls.ensure((size_t)ls_blocks() * 2 * sizeof(double));
-      ss->part_up.ensure((size_t)ls_blocks() * sizeof(double));
-      ss->dots.ensure((size_t)(finish_max_blocks() + 1) * 2 * sizeof(double));
-      plan->ensure_T(focus->nk + defocus->nk);
+      ck(cudaMemcpyAsync(ss->target.p, target_dev, n, cudaMemcpyDeviceToDevice, s), "memcpy");
       // optimizer.py:197-201: uniform target -> DegenerateInputError
       {
-        DevBuf zero;
-        zero.ensure(n);
-        ck(cudaMemsetAsync(zero.p, 0, n, s), "memset");
-        double lit = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, ss->target.as<uint8_t>(), zero.as<uint8_t>(),
-                                    plan, s);
-        zero.release();
+        double lit = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, ss->target.as<uint8_t>(), nullptr, plan, s);
         if (lit == 0.0 || lit == (double)n) throw Error(LSOPC_EDEGENERATE, "target layout is uniform");
       }
       if (phi0_dev) {
@@ -547,18 +612,34 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
                     plan->tsdf_i.as<int>(), plan->tsdf_f.as<double>(), s);
         ck_launch("tsdf");
       }
-      if (mod_dev) {
-        ss->have_mod = true;
-        ss->mod.ensure(n * 8);
-        ck(cudaMemcpyAsync(ss->mod.p, mod_dev, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
-      }
+      if (mod_dev) ck(cudaMemcpyAsync(ss->mod.p, mod_dev, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
       ck(cudaMemcpyAsync(ss->best.p, ss->phi.p, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
       launch_elementwise(EW_MASK, n, ss->phi.as<double>(), nullptr, 0, 0, 0, nullptr, ss->mask.as<uint8_t>(), s);
       DevState h{};
       h.best = std::numeric_limits<double>::infinity();
       h.nonfinite_it = -1;
       ck(cudaMemcpyAsync(ss->state.p, &h, sizeof(h), cudaMemcpyHostToDevice, s), "memcpy");
+      for (int i = 0; i < 2; ++i) ck(cudaMemsetAsync(ss->v[i].p, 0, n * 8, s), "memset");
       ck(cudaStreamSynchronize(s), "sync");
+      // capture the two parities on a private stream (the caller's may be the legacy stream)
+      const char* ng = std::getenv("LSOPC_B200_NO_GRAPH");
+      if (fresh && !(ng && ng[0] == '1')) {
+      cudaStream_t cs;
+      ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
+      for (int par = 0; par < 2; ++par) {
+        cudaGraph_t gr;
+        ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed), "capture");
+        enqueue_iteration(ss, par, cs);
+        ck(cudaStreamEndCapture(cs, &gr), "capture end");
+        ck(cudaGraphInstantiate(&ss->graph[par], gr, 0), "graph instantiate");
+        cudaGraphDestroy(gr);
+      }
+      cudaStreamDestroy(cs);
+      }
+      if (fresh) {
+        ck(cudaHostAlloc(&ss->hflag, 2 * sizeof(int), cudaHostAllocDefault), "host alloc");
+        for (auto& e : ss->ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      }
     } catch (...) {
       delete ss;
       throw;
@@ -570,7 +651,11 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
 int lsopc_session_enqueue(lsopc_session* ss, int n) {
   return guarded([&] {
     if (!ss) throw Error(LSOPC_EINVAL, "null session");
-    for (int i = 0; i < n && ss->it < ss->cfg.max_iters; ++i) enqueue_iteration(ss, ss->it++);
+    for (int i = 0; i < n && ss->it < ss->cfg.max_iters; ++i) {
+      if (ss->graph[ss->it & 1]) ck(cudaGraphLaunch(ss->graph[ss->it & 1], ss->s), "graph launch");
+      else enqueue_iteration(ss, ss->it & 1, ss->s);
+      ++ss->it;
+    }
   });
 }
 
@@ -633,8 +718,9 @@ int lsopc_session_phi(lsopc_session* ss, double* phi_dev) {
 
 int lsopc_session_destroy(lsopc_session* ss) {
   return guarded([&] {
-    if (ss) cudaStreamSynchronize(ss->s);
-    delete ss;
+    if (!ss) return;
+    ck(cudaStreamSynchronize(ss->s), "sync");
+    give_to_pool(ss);
   });
 }
 
@@ -646,7 +732,8 @@ int lsopc_session_time_passes(lsopc_session* ss, int reps, double* ms_out) {
     for (auto& e : ev) ck(cudaEventCreate(&e), "event");
     double acc[PS_N] = {0};
     for (int r = 0; r < reps && ss->it < ss->cfg.max_iters; ++r) {
-      enqueue_iteration(ss, ss->it++, ev);
+      enqueue_iteration(ss, ss->it & 1, ss->s, ev);
+      ++ss->it;
       ck(cudaEventSynchronize(ev[PS_N]), "sync");
       for (int i = 0; i < PS_N; ++i) {
         float ms = 0.f;
@@ -672,14 +759,27 @@ int lsopc_optimize(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_kset* 
   lsopc_session* ss = nullptr;
   int rc = lsopc_session_create(plan, focus, defocus, target_dev, phi0_dev, mod_dev, cfg, stream, &ss);
   if (rc) return rc;
-  int chunk = 2;
-  while (true) {
-    rc = lsopc_session_enqueue(ss, chunk);
-    if (rc) break;
-    int stopped = 0, enq = 0;
-    rc = lsopc_session_poll(ss, &stopped, &enq);
-    if (rc || stopped || enq >= cfg->max_iters) break;
-    if (chunk < 8) chunk *= 2;
+  // Keep one chunk queued ahead: enqueue chunk k+1, then wait for chunk k and
+  // read its stop flag (copied to pinned memory behind it).  Once the device
+  // stop rule fires, every later kernel exits at entry, so over-enqueueing
+  // costs at most one chunk of empty launches.
+  const int chunk = 4;
+  auto enqueue_chunk = [&](int slot) -> int {
+    int r = lsopc_session_enqueue(ss, chunk);
+    if (r) return r;
+    r = guarded([&] {
+      ck(cudaMemcpyAsync(&ss->hflag[slot], &ss->st()->stopped, sizeof(int), cudaMemcpyDeviceToHost, ss->s),
+         "memcpy");
+      ck(cudaEventRecord(ss->ev[slot], ss->s), "event");
+    });
+    return r;
+  };
+  rc = enqueue_chunk(0);
+  for (int k = 0; !rc; ++k) {
+    const bool more = ss->it < cfg->max_iters;
+    if (more && (rc = enqueue_chunk((k + 1) & 1))) break;
+    rc = guarded([&] { ck(cudaEventSynchronize(ss->ev[k & 1]), "sync"); });
+    if (rc || ss->hflag[k & 1] || !more) break;
   }
   if (!rc) rc = lsopc_session_finish(ss, best_phi_dev, final_mask_dev, history_host, result);
   std::string keep = g_err;

@@ -281,9 +281,15 @@ def optimize(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=
                                      nv.ptr(mdv), ctypes.byref(c), nv.ptr(best), nv.ptr(fmask),
                                      hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res),
                                      nv.stream()))
+    # device -> host through a pinned staging buffer; wall_time is taken before
+    # the shot count, as in the reference (optimizer.py:274-281)
     final_mask = nv.to_host(fmask)
-    best_phi = nv.to_host(best)
+    stage = nv.pinned_like(best)
+    stage.copy_(best, non_blocking=True)
+    nv.torch().cuda.current_stream().synchronize()
+    best_phi = stage.numpy().copy()
     wall = time.perf_counter() - t0
+    shots = shot_count(final_mask)
     history = [IterationRecord(*(float(v) for v in row)) for row in hist[:res.iters]]
     bounds = (cfg.d_upper, cfg.d_lower)
     if phi0 is not None:
@@ -292,8 +298,7 @@ def optimize(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=
         losses = [h.l_dso for h in history]
         if not losses or int(np.argmin(losses)) == 0:
             bounds = (phi0.d_upper, phi0.d_lower)
-    report = MetricsReport(l2=res.l2, pvband=res.pvband, shots=shot_count(final_mask),
-                           wall_time=wall, iters=res.iters)
+    report = MetricsReport(l2=res.l2, pvband=res.pvband, shots=shots, wall_time=wall, iters=res.iters)
     return OptimizationResult(final_mask=final_mask,
                               final_phi=LevelSetField(best_phi, bounds[0], bounds[1]),
                               metrics=report, loss_history=history, iters_run=res.iters,
