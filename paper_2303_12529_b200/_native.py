@@ -17,7 +17,8 @@ import numpy as np
 
 from .errors import DegenerateInputError, NumericalError
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "liblsopc_b200.so"
+_LIB_PATH = Path(os.environ.get("LSOPC_B200_LIB") or
+                 Path(__file__).resolve().parent / "_lib" / "liblsopc_b200.so")
 
 OK, EINVAL, EDEGENERATE, ENUMERIC, ECUDA = 0, 1, 2, 3, 4
 FP32, FP64 = 0, 1

@@ -17,8 +17,12 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-OUT_DIR = PKG / "_lib"
+# LSB_OUT / LSB_DEFINES build experiment variants into another directory
+# (e.g. LSB_OUT=/tmp/v1 LSB_DEFINES="-DLSB_EXP_NOSTORE"); the package loads
+# the default library unless LSOPC_B200_LIB points elsewhere.
+OUT_DIR = Path(os.environ.get("LSB_OUT") or (PKG / "_lib"))
 LIB = OUT_DIR / "liblsopc_b200.so"
+EXTRA = os.environ.get("LSB_DEFINES", "").split()
 INCLUDE = PKG.parent / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -37,7 +41,7 @@ def _headers_mtime():
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    OUT_DIR.mkdir(exist_ok=True)
+    OUT_DIR.mkdir(parents=True, exist_ok=True)
     hdr = _headers_mtime()
     objs, jobs = [], []
     for src in _sources():
@@ -48,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(job):
         src, obj = job
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -31,9 +31,14 @@
 #include "common.cuh"
 #include "engine.cuh"
 #include "internal.h"
+#include "tma.cuh"
+
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
+#include <string>
 
 namespace lsb {
 namespace spec {
@@ -96,7 +101,9 @@ template <typename R, class Op>
 __global__ void __launch_bounds__(512, 1) k_pass(Op op, StopFlag stop) {
   using C = typename CT<R>::C;
   constexpr int NB = Op::kStages;  // ring of stage buffers: prefetch distance NB - 1
+#if !defined(LSB_EXP_NOSTORE) && !defined(LSB_EXP_NOGATHER)
   if (stop && *stop) return;
+#endif
   extern __shared__ __align__(16) unsigned char smraw[];
   C* const base = reinterpret_cast<C*>(smraw);
   C* extra = base + NB * op.bufE;
@@ -110,14 +117,18 @@ __global__ void __launch_bounds__(512, 1) k_pass(Op op, StopFlag stop) {
   int pit = it, pst = st;  // next (item, step) to prefetch
 #pragma unroll
   for (int d = 0; d < NB - 1; ++d) {
+#ifndef LSB_EXP_NOGATHER  // experiment switch: never fetch operands
     if (pit < op.nitems) op.prefetch(pit, pst, base + d * op.bufE, extra);
+#endif
     eng::cp_commit();
     if (pit < op.nitems) advance(pit, pst);
   }
   int slot = 0;  // ring slot of (it, st)
   while (true) {
     const int pslot = slot == 0 ? NB - 1 : slot - 1;  // == (slot + NB - 1) % NB
+#ifndef LSB_EXP_NOGATHER
     if (pit < op.nitems) op.prefetch(pit, pst, base + pslot * op.bufE, extra);
+#endif
     eng::cp_commit();
     eng::cp_wait<NB - 1>();
     __syncthreads();
@@ -143,6 +154,16 @@ struct OpBase {
   template <class S, class C> LS_D void end(S&, int, C*, C*) const {}
   template <class S> LS_D void finish(S&, double*) const {}
 };
+
+// Global stores of the transform outputs.  LSB_EXP_NOSTORE (experiment
+// builds only) keeps the arithmetic but drops the writes.
+template <class T> LS_D void gstore(T& dst, const T& v) {
+#ifdef LSB_EXP_NOSTORE
+  if (v.x == (decltype(v.x))1.2345e-30) dst = v;
+#else
+  dst = v;
+#endif
+}
 
 // ---- address helpers: idx = j + r*STRIDE (STRIDE == 0: generic path, idx = j)
 
@@ -217,7 +238,7 @@ template <typename R> struct MaskRowsOp : OpBase {
       }
       return cmk(m, (R)0);
     }
-    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_row<LGN, ST, C>(L, y0 + seq, j, r)] = v; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { gstore(out[ct_row<LGN, ST, C>(L, y0 + seq, j, r)], v); }
   };
   template <class St> LS_D void step(St&, int it, int, C* b, C*) const {
     const Geo g = sh.grow();
@@ -359,7 +380,7 @@ template <typename R> struct F1Op : OpBase {
       else return cmul(mhat[Lm.at(j, x0 + seq)], x) * scale;
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
-      out[ct_col<LGN, ST, C, kLgTileT>(L, j, r, x0 + seq)] = v;
+      gstore(out[ct_col<LGN, ST, C, kLgTileT>(L, j, r, x0 + seq)], v);
     }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
@@ -402,7 +423,7 @@ template <typename R> struct F2Op : OpBase {
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_row<LGN, ST>(seq, j, r, lgn)]; }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int slot) {
       S.acc[slot] += w * (v.x * v.x + v.y * v.y);
-      A[rm_row<LGN, ST>(W, y0 + seq, j, r)] = v;
+      gstore(A[rm_row<LGN, ST>(W, y0 + seq, j, r)], v);
     }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
@@ -475,7 +496,7 @@ template <typename R> struct A1Op : OpBase {
       if constexpr (LGN > 0) return x * S.g[slot];
       else return x * gate[(size_t)(y0 + seq) * W + j];
     }
-    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_row<LGN, ST, C>(L, y0 + seq, j, r)] = v; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { gstore(out[ct_row<LGN, ST, C>(L, y0 + seq, j, r)], v); }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
     const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
@@ -624,6 +645,332 @@ template <typename R> struct A3Op : OpBase {
   }
 };
 
+// ===========================================================================
+// TMA variants of the four kernel-looping passes.
+//
+// Same arithmetic as F1Op / F2Op / A1Op / A2Op; operands arrive by TMA
+// (1-D bulk copies of contiguous rows / tiles, 4-D tensor copies for the
+// column-tiled fields) into a 3-slot ring guarded by mbarriers, and the
+// per-kernel output tile is written to shared memory by the last butterfly
+// stage and streamed out by TMA stores.  Slot roles at step q: q%3 is being
+// transformed, (q+1)%3 is being filled, (q+2)%3 == (q-1)%3 drains the
+// previous step's stores.  No thread issues per-element global loads or
+// stores of the streamed fields, so the LSU only serves the exchange.
+
+// field layout seen by TMA: 8-byte words, dims {w*EW, W/w, H, NK}
+struct TmaField {
+  const void* base;
+  int lgw;   // tile width (elements)
+  int ew;    // 8-byte words per element (1: complex64, 2: complex128)
+};
+
+inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled is unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// map over NK column-tiled fields of H x W elements; box in words/tiles/rows
+inline CUtensorMap make_field_map(const TmaField& f, int H, int W, int NK, unsigned b0, unsigned b1, unsigned b2) {
+  const uint64_t w = 1ull << f.lgw, es = 8ull * f.ew;
+  cuuint64_t dim[4] = {w * f.ew, (uint64_t)W >> f.lgw, (uint64_t)H, (uint64_t)NK};
+  cuuint64_t stride[3] = {(uint64_t)H * w * es, w * es, (uint64_t)H * W * es};
+  cuuint32_t box[4] = {b0, b1, b2, 1};
+  cuuint32_t est[4] = {1, 1, 1, 1};
+  CUtensorMap m;
+  CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(f.base), dim, stride, box, est,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+// TMA path usable for this geometry (fast path, 16 B box rows, box <= 256)
+template <typename R> bool tma_ok(const Shape<R>& sh) {
+  using C = typename CT<R>::C;
+  static const bool off = [] {
+    const char* e = std::getenv("LSOPC_B200_NO_TMA");
+    return e && e[0] == '1';
+  }();
+  if (off || !sh.fast()) return false;
+  // the TMA op bodies exist only for the compile-time FFT geometry (eng::dispatch)
+  constexpr int LGE = eng::lg_full<C>();
+  if (sh.lgH < eng::kFastMinLgn || sh.lgW < eng::kFastMinLgn || sh.lgS != LGE - sh.lgH || sh.lgR != LGE - sh.lgW)
+    return false;
+  const int ew = sizeof(C) / 8;
+  const int S = 1 << sh.lgS, w = 1 << lg_tile<C>();
+  return std::min(S, w) * ew * 8 >= 16 && S % std::min(S, w) == 0;
+}
+
+template <typename R, class Op>
+__global__ void __launch_bounds__(512, 1) k_pass_tma(const __grid_constant__ Op op, StopFlag stop) {
+  using C = typename CT<R>::C;
+#if !defined(LSB_EXP_NOSTORE) && !defined(LSB_EXP_NOGATHER)
+  if (stop && *stop) return;
+#endif
+  extern __shared__ __align__(128) unsigned char smraw[];
+  C* const base = reinterpret_cast<C*>(smraw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 3 * (size_t)op.bufE * sizeof(C));
+  typename Op::State S{};
+  if ((int)blockIdx.x >= op.nitems) return;
+  const bool leader = threadIdx.x == 0;
+  if (leader) {
+    for (int i = 0; i < 3; ++i) tma::mbar_init(&bar[i], 1);
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  auto advance = [&](int& it, int& st) {
+    if (++st == op.steps(it)) { st = 0; it += gridDim.x; }
+  };
+  int it = blockIdx.x, st = 0;
+  int nit = it, nst = st;  // next step to load
+  if (leader) {
+    tma::mbar_expect_tx(&bar[0], op.load_bytes());
+    op.load(nit, nst, base, &bar[0]);
+  }
+  advance(nit, nst);
+  for (unsigned q = 0;; ++q) {
+    const int slot = q % 3, nslot = (q + 1) % 3;
+    if (leader && nit < op.nitems) {
+      if (Op::kStores) tma::bulk_wait_read<1>();  // slot nslot held the stores of step q-2
+      tma::mbar_expect_tx(&bar[nslot], op.load_bytes());
+      op.load(nit, nst, base + nslot * op.bufE, &bar[nslot]);
+    }
+    tma::mbar_wait(&bar[slot], (q / 3) & 1);
+    C* const cur = base + slot * op.bufE;
+    if (st == 0) op.begin(S, it, cur);
+    op.step(S, it, st, cur, cur);
+    if (Op::kStores) {
+      tma::fence_async_smem();
+      __syncthreads();
+      if (leader) {
+        op.store(it, st, cur);
+        tma::bulk_commit();
+      }
+    } else {
+      __syncthreads();
+    }
+    if (st == op.steps(it) - 1) op.end(S, it, cur, cur);
+    if (nit < op.nitems) advance(nit, nst);
+    advance(it, st);
+    if (it >= op.nitems) break;
+  }
+  if (leader && Op::kStores) tma::bulk_wait<0>();
+  op.finish(S, reinterpret_cast<double*>(smraw));
+}
+
+// natural (dense) output position in a buffer; the TMA store box order
+template <int LGN, int STRIDE, typename C, bool COLS> LS_D int nat_out(int seq, int j, int r) {
+  if constexpr (COLS) return nat_col<LGN, STRIDE, C>(seq, j, r, 0);
+  else return nat_row<LGN, STRIDE>(seq, j, r, 0);
+}
+
+// TF1: T_k = IFFT_y(M^ . H_k)/(HW); H_k tile in by TMA, T_k slab out by TMA
+template <typename R> struct TF1Op : OpBase {
+  using C = typename CT<R>::C;
+  static constexpr int P = eng::P_of<C>();
+  static constexpr bool kStores = true;
+  using State = typename F1Op<R>::State;
+  Shape<R> sh;
+  SetArgs<R> a;
+  const C* mhat;
+  R scale;
+  const C* tw;
+  int lgnt;
+  int spec_lgw;                    // tile width of the spectra layout
+  alignas(64) CUtensorMap tmap_spec;   // spectra of set 0, column-item boxes
+  alignas(64) CUtensorMap tmap_spec1;  // spectra of set 1
+  alignas(64) CUtensorMap tmap_T;     // T fields, column-item boxes
+  int koff[2];                      // first kernel index of each set in the stacked maps
+  LS_D int steps(int it) const { return a.nk[it >> lgnt]; }
+  LS_D unsigned load_bytes() const { return (unsigned)((sh.H << sh.lgS) * sizeof(C)); }
+  LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
+    const int set = it >> lgnt, x0 = (it & ((1 << lgnt) - 1)) << sh.lgS;
+    const CUtensorMap* m = set ? &tmap_spec1 : &tmap_spec;
+    col_boxes(x0, k, spec_lgw, [&](int c0, int c1, int c2, int kk, int off) {
+      tma::tensor_g2s(dst + off, m, c0, c1, c2, kk, bar);
+    });
+  }
+  LS_D void store(int it, int k, const C* src) const {
+    const int set = it >> lgnt, x0 = (it & ((1 << lgnt) - 1)) << sh.lgS;
+    col_boxes(x0, k + koff[set], kLgTileT, [&](int c0, int c1, int c2, int kk, int off) {
+      tma::tensor_s2g(&tmap_T, c0, c1, c2, kk, src + off);
+    });
+  }
+  // boxes of a column item: {min(S,w) words-per-elem, S/w tiles, 256 rows}
+  template <class Fn> LS_D void col_boxes(int x0, int kk, int lgw, Fn&& fn) const {
+    const int ew = sizeof(C) / 8, w = 1 << lgw, S = 1 << sh.lgS;
+    const int rows = sh.H < 256 ? sh.H : 256;
+    for (int b = 0; b * rows < sh.H; ++b) fn((x0 & (w - 1)) * ew, x0 >> lgw, b * rows, kk, b * rows * S);
+  }
+  LS_D void begin(State& S, int it, C*) const {
+    const int t = it & ((1 << lgnt) - 1);
+    eng::dispatch<C>(sh.gcol(), true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0)
+        eng::for_first_slots<LGN, true, C>(typename F1Op<R>::template LoadM<LGN>{S, mhat, sh.ct(), t << sh.lgS});
+    });
+  }
+  template <int LGN> struct F {
+    C* b;
+    const State& S;
+    R scale;
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
+      return cmul(S.mh[slot], b[nat_col<LGN, ST, C>(seq, j, r, 0)]) * scale;
+    }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, true>(seq, j, r)] = v; }
+  };
+  LS_D void step(State& S, int, int, C* b, C*) const {
+    const Geo g = sh.gcol();
+    eng::dispatch<C>(g, true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) {
+        F<LGN> f{b, S, scale};
+        eng::run_fix<LGN, true, true>(g, b, tw, f);
+      }
+    });
+  }
+};
+
+// TF2: A_k = IFFT_x T_k (out by 1-D bulk), I_set = sum w |A_k|^2 (registers)
+template <typename R> struct TF2Op : OpBase {
+  using C = typename CT<R>::C;
+  static constexpr int P = eng::P_of<C>();
+  static constexpr bool kStores = true;
+  using State = typename F2Op<R>::State;
+  Shape<R> sh;
+  SetArgs<R> a;
+  const C* tw;
+  int lgnb;
+  alignas(64) CUtensorMap tmap_T;  // T fields, row-item boxes
+  int koff[2];
+  LS_D int steps(int it) const { return a.nk[it >> lgnb]; }
+  LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
+  LS_D unsigned load_bytes() const { return (unsigned)((sh.W << sh.lgR) * sizeof(C)); }
+  LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
+    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int tiles = sh.W >> kLgTileT, bt = tiles < 256 ? tiles : 256;
+    for (int r = 0; r < (1 << sh.lgR); ++r)
+      for (int b = 0; b * bt < tiles; ++b)
+        tma::tensor_g2s(dst + (r << sh.lgW) + ((b * bt) << kLgTileT), &tmap_T, 0, b * bt, y0 + r, k + koff[set], bar);
+  }
+  LS_D void store(int it, int k, const C* src) const {
+    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    tma::bulk_s2g(a.A[set] + (size_t)k * fsz() + ((size_t)y0 << sh.lgW), src, load_bytes());
+  }
+  LS_D void begin(State& S, int, C*) const {
+#pragma unroll
+    for (int i = 0; i < P; ++i) S.acc[i] = (R)0;
+  }
+  template <int LGN> struct F {
+    C* b;
+    State& S;
+    R w;
+    template <int ST> LS_D C load(int seq, int j, int r, int) const { return b[nat_row<LGN, ST>(seq, j, r, 0)]; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int slot) {
+      S.acc[slot] += w * (v.x * v.x + v.y * v.y);
+      b[nat_out<LGN, ST, C, false>(seq, j, r)] = v;
+    }
+  };
+  LS_D void step(State& S, int it, int k, C* b, C*) const {
+    const Geo g = sh.grow();
+    eng::dispatch<C>(g, true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) {
+        F<LGN> f{b, S, a.w[it >> lgnb][k]};
+        eng::run_fix<LGN, false, true>(g, b, tw, f);
+      }
+    });
+  }
+  LS_D void end(State& S, int it, C*, C*) const {
+    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const Geo g = sh.grow();
+    eng::dispatch<C>(g, true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      eng::for_last_slots<LGN, false, C>(g, typename F2Op<R>::template WriteI<LGN>{a.I[set], S, y0, sh.W});
+    });
+  }
+};
+
+// TA1: U_k = FFT_x(gate . A_k): A_k rows in by 1-D bulk, U_k rows out by tensor map
+template <typename R> struct TA1Op : OpBase {
+  using C = typename CT<R>::C;
+  static constexpr int P = eng::P_of<C>();
+  static constexpr bool kStores = true;
+  using State = typename A1Op<R>::State;
+  Shape<R> sh;
+  SetArgs<R> a;
+  const C* tw;
+  int lgnb;
+  alignas(64) CUtensorMap tmap_U;  // U fields (layout tile lg_tile<C>), row-item boxes
+  int koff[2];
+  LS_D int steps(int it) const { return a.nk[it >> lgnb]; }
+  LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
+  LS_D unsigned load_bytes() const { return (unsigned)((sh.W << sh.lgR) * sizeof(C)); }
+  LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
+    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    tma::bulk_g2s(dst, a.A[set] + (size_t)k * fsz() + ((size_t)y0 << sh.lgW), load_bytes(), bar);
+  }
+  LS_D void store(int it, int k, const C* src) const {
+    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    constexpr int LGT = lg_tile<C>();
+    const int tiles = sh.W >> LGT, bt = tiles < 256 ? tiles : 256;
+    for (int r = 0; r < (1 << sh.lgR); ++r)
+      for (int b = 0; b * bt < tiles; ++b)
+        tma::tensor_s2g(&tmap_U, 0, b * bt, y0 + r, k + koff[set], src + (r << sh.lgW) + ((b * bt) << LGT));
+  }
+  LS_D void begin(State& S, int it, C*) const {
+    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    eng::dispatch<C>(sh.grow(), true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0)
+        eng::for_first_slots<LGN, false, C>(typename A1Op<R>::template LoadG<LGN>{S, a.gate[set], y0, sh.W});
+    });
+  }
+  template <int LGN> struct F {
+    C* b;
+    const State& S;
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
+      return b[nat_row<LGN, ST>(seq, j, r, 0)] * S.g[slot];
+    }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, false>(seq, j, r)] = v; }
+  };
+  LS_D void step(State& S, int, int, C* b, C*) const {
+    const Geo g = sh.grow();
+    eng::dispatch<C>(g, true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) {
+        F<LGN> f{b, S};
+        eng::run_fix<LGN, false, false>(g, b, tw, f);
+      }
+    });
+  }
+};
+
+// TA2: V_set = IFFT_y(sum_k w_k conj(H_k) FFT_y U_k): U_k tile in by TMA
+template <typename R> struct TA2Op : A2Op<R> {
+  using C = typename CT<R>::C;
+  static constexpr bool kStores = false;
+  int u_lgw;
+  alignas(64) CUtensorMap tmap_U;  // U fields, column-item boxes
+  int koff[2];
+  LS_D unsigned load_bytes() const { return (unsigned)((this->sh.H << this->sh.lgS) * sizeof(C)); }
+  LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
+    const int set = it >> this->lgnt, x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
+    const int ew = sizeof(C) / 8, w = 1 << u_lgw, S = 1 << this->sh.lgS;
+    const int rows = this->sh.H < 256 ? this->sh.H : 256;
+    for (int b = 0; b * rows < this->sh.H; ++b)
+      tma::tensor_g2s(dst + b * rows * S, &tmap_U, (x0 & (w - 1)) * ew, x0 >> u_lgw, b * rows, k + koff[set], bar);
+  }
+  LS_D void store(int, int, const C*) const {}
+};
+
 // ---------------------------------------------------------------------------
 // launch plumbing
 
@@ -663,6 +1010,37 @@ int launch_op(Op& op, int threads, int extra_bufs, StopFlag stop, cudaStream_t s
   kern<<<grid, threads, smem, s>>>(op, stop);
   return grid;
 }
+
+template <typename R, class Op>
+int launch_tma(Op& op, int threads, StopFlag stop, cudaStream_t s) {
+  using C = typename CT<R>::C;
+  const size_t smem = 3 * (size_t)op.bufE * sizeof(C) + 3 * sizeof(uint64_t);
+  if (smem > 227 * 1024) throw std::runtime_error("TMA pass needs more than 227 KB of shared memory");
+  auto kern = k_pass_tma<R, Op>;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem);
+    per_sm = std::max(b, 1);
+  }
+  const int grid = std::max(1, std::min(op.nitems, num_sms() * per_sm));
+  kern<<<grid, threads, smem, s>>>(op, stop);
+  return grid;
+}
+
+// slot size for the TMA ring: the padded exchange buffer, rounded to 128 B
+template <typename R> int tma_bufE(int e) {
+  using C = typename CT<R>::C;
+  const int q = 128 / (int)sizeof(C);
+  return (e + q - 1) / q * q;
+}
+
+template <typename R> int set_koff(const SetArgs<R>& a, int set, size_t n) {
+  return (int)((a.T[set] - a.T[0]) / (std::ptrdiff_t)n);
+}
+template <typename R> int total_nk(const SetArgs<R>& a) { return a.nk[0] + (a.nsets > 1 ? a.nk[1] : 0); }
 
 template <typename R> int col_threads(const Shape<R>& sh) {
   using C = typename CT<R>::C;
@@ -734,6 +1112,32 @@ void f1_impl(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, St
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
+  if (tma_ok(sh)) {
+    TF1Op<R> f1;
+    f1.sh = sh;
+    f1.a = a;
+    f1.mhat = static_cast<const C*>(mhat);
+    f1.scale = (R)(1.0 / (double)g.n());
+    f1.tw = static_cast<const C*>(g.tw);
+    f1.lgnt = g.lgW - sh.lgS;
+    f1.spec_lgw = sh.lgT;
+    const int ew = sizeof(C) / 8, S = 1 << sh.lgS, rows = std::min(g.H, 256);
+    auto colbox = [&](int lgw) { return std::make_pair((unsigned)(std::min(S, 1 << lgw) * ew),
+                                                         (unsigned)std::max(1, S >> lgw)); };
+    // spectra of each set: separate allocations -> separate maps (koff 0)
+    for (int i = 0; i < nsets; ++i) {
+      auto cb = colbox(sh.lgT);
+      CUtensorMap m = make_field_map(TmaField{a.spec[i], sh.lgT, ew}, g.H, g.W, a.nk[i], cb.first, cb.second, rows);
+      if (i == 0) f1.tmap_spec = m; else f1.tmap_spec1 = m;
+    }
+    auto cbT = colbox(kLgTileT);
+    f1.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), cbT.first, cbT.second, rows);
+    for (int i = 0; i < 2; ++i) f1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+    f1.bufE = tma_bufE<R>(col_bufE(sh));
+    f1.nitems = (1 << f1.lgnt) * nsets;
+    launch_tma<R>(f1, col_threads(sh), stop, s);
+    return;
+  }
   F1Op<R> f1;
   f1.sh = sh;
   f1.a = a;
@@ -751,14 +1155,29 @@ void f2_impl(const Grid& g, const SpecSet* sets, int nsets, double2* a0_out, Sto
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
-  F2Op<R> f2;
-  f2.sh = sh;
-  f2.a = a;
-  f2.tw = static_cast<const C*>(g.tw);
-  f2.lgnb = g.lgH - sh.lgR;
-  f2.bufE = row_bufE(sh);
-  f2.nitems = (1 << f2.lgnb) * nsets;
-  launch_op<R>(f2, row_threads(sh), 0, stop, s);
+  if (tma_ok(sh)) {
+    TF2Op<R> f2;
+    f2.sh = sh;
+    f2.a = a;
+    f2.tw = static_cast<const C*>(g.tw);
+    f2.lgnb = g.lgH - sh.lgR;
+    const int ew = sizeof(C) / 8, tiles = g.W >> kLgTileT;
+    f2.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), (unsigned)((1 << kLgTileT) * ew),
+                               (unsigned)std::min(tiles, 256), 1);
+    for (int i = 0; i < 2; ++i) f2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+    f2.bufE = tma_bufE<R>(row_bufE(sh));
+    f2.nitems = (1 << f2.lgnb) * nsets;
+    launch_tma<R>(f2, row_threads(sh), stop, s);
+  } else {
+    F2Op<R> f2;
+    f2.sh = sh;
+    f2.a = a;
+    f2.tw = static_cast<const C*>(g.tw);
+    f2.lgnb = g.lgH - sh.lgR;
+    f2.bufE = row_bufE(sh);
+    f2.nitems = (1 << f2.lgnb) * nsets;
+    launch_op<R>(f2, row_threads(sh), 0, stop, s);
+  }
   if (a0_out)  // convolve(): the first set's first field A_0
     k_ct_to_c128<R><<<148 * 4, 256, 0, s>>>(g.n(), sh.rm(), g.W, a.A[0], a0_out);
 }
@@ -768,6 +1187,21 @@ void a1_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
+  if (tma_ok(sh)) {
+    TA1Op<R> a1;
+    a1.sh = sh;
+    a1.a = a;
+    a1.tw = static_cast<const C*>(g.tw);
+    a1.lgnb = g.lgH - sh.lgR;
+    const int ew = sizeof(C) / 8, tiles = g.W >> sh.lgT;
+    a1.tmap_U = make_field_map(TmaField{a.T[0], sh.lgT, ew}, g.H, g.W, total_nk(a), (unsigned)((1 << sh.lgT) * ew),
+                               (unsigned)std::min(tiles, 256), 1);
+    for (int i = 0; i < 2; ++i) a1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+    a1.bufE = tma_bufE<R>(row_bufE(sh));
+    a1.nitems = (1 << a1.lgnb) * nsets;
+    launch_tma<R>(a1, row_threads(sh), stop, s);
+    return;
+  }
   A1Op<R> a1;
   a1.sh = sh;
   a1.a = a;
@@ -783,6 +1217,22 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
+  if (tma_ok(sh)) {
+    TA2Op<R> a2;
+    a2.sh = sh;
+    a2.a = a;
+    a2.tw = static_cast<const C*>(g.tw);
+    a2.lgnt = g.lgW - sh.lgS;
+    a2.u_lgw = sh.lgT;
+    const int ew = sizeof(C) / 8, S = 1 << sh.lgS, w = 1 << sh.lgT;
+    a2.tmap_U = make_field_map(TmaField{a.T[0], sh.lgT, ew}, g.H, g.W, total_nk(a), (unsigned)(std::min(S, w) * ew),
+                               (unsigned)std::max(1, S / w), (unsigned)std::min(g.H, 256));
+    for (int i = 0; i < 2; ++i) a2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+    a2.bufE = tma_bufE<R>(col_bufE(sh));
+    a2.nitems = (1 << a2.lgnt) * nsets;
+    launch_tma<R>(a2, col_threads(sh), stop, s);
+    return;
+  }
   A2Op<R> a2;
   a2.sh = sh;
   a2.a = a;
