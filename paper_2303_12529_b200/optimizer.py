@@ -262,10 +262,11 @@ def _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation):
     return target, m, fk, dk
 
 
-def optimize(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=None):
-    """Full level-set ILT loop on the device (optimizer.py:204-284).  Returns
-    the lowest-loss iterate, binarised, with hard-resist metrics and the loss
-    history."""
+def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=None):
+    """Device part of `optimize`: the loop, final prints and the device-to-host
+    copies.  Returns the pieces `_assemble` turns into an OptimizationResult
+    (split so a batch driver can overlap one clip's host tail with the next
+    clip's device loop)."""
     t0 = time.perf_counter()
     target, m, fk, dk = _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
     shape = target.shape
@@ -289,8 +290,14 @@ def optimize(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=
     nv.torch().cuda.current_stream().synchronize()
     best_phi = stage.numpy().copy()
     wall = time.perf_counter() - t0
+    return final_mask, best_phi, (res.iters, res.l2, res.pvband), hist, wall
+
+
+def _assemble(parts, cfg, phi0=None):
+    """Host tail of `optimize`: shot count, history records, result."""
+    final_mask, best_phi, (iters, l2, pvb), hist, wall = parts
     shots = shot_count(final_mask)
-    history = [IterationRecord(*(float(v) for v in row)) for row in hist[:res.iters]]
+    history = [IterationRecord(*(float(v) for v in row)) for row in hist[:iters]]
     bounds = (cfg.d_upper, cfg.d_lower)
     if phi0 is not None:
         # the initial iterate keeps phi0's own bounds (optimizer.py:219-220,231);
@@ -298,11 +305,19 @@ def optimize(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=
         losses = [h.l_dso for h in history]
         if not losses or int(np.argmin(losses)) == 0:
             bounds = (phi0.d_upper, phi0.d_lower)
-    report = MetricsReport(l2=res.l2, pvband=res.pvband, shots=shots, wall_time=wall, iters=res.iters)
+    report = MetricsReport(l2=l2, pvband=pvb, shots=shots, wall_time=wall, iters=iters)
     return OptimizationResult(final_mask=final_mask,
                               final_phi=LevelSetField(best_phi, bounds[0], bounds[1]),
-                              metrics=report, loss_history=history, iters_run=res.iters,
+                              metrics=report, loss_history=history, iters_run=iters,
                               wall_time=wall)
+
+
+def optimize(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=None):
+    """Full level-set ILT loop on the device (optimizer.py:204-284).  Returns
+    the lowest-loss iterate, binarised, with hard-resist metrics and the loss
+    history."""
+    parts = _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
+    return _assemble(parts, cfg, phi0)
 
 
 @dataclass

@@ -73,22 +73,39 @@ def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, sol
     owns it.  Returns (records of all clips ordered by index,
     seconds = max over ranks of this rank's solve time).
 
-    `solver(target, focus, defocus, cfg) -> OptimizationResult` defaults to
-    `optimizer.optimize` (the device loop); tests inject a stub.
+    `solver(target, focus, defocus, cfg) -> OptimizationResult` replaces the
+    device loop (tests inject a stub).  Without it, clips run through
+    `optimizer.optimize`'s two halves, with each clip's host tail (shot count,
+    records) overlapping the next clip's device loop.
     """
-    if solver is None:
-        from .optimizer import optimize as solver
     rank, world = world_info(group)
     mine = [(i, targets[i]) for i in shard(len(targets), rank, world)]  # inputs built before timing
     if synchronize:
         synchronize()
     t0 = time.perf_counter()
     records = []
-    for i, target in mine:
-        r = solver(target, focus_kernels, defocus_kernels, cfg)
+
+    def record(i, r):
         m = r.metrics
         records.append(ClipRecord(i, rank, int(m.l2), int(m.pvband), int(m.shots), int(r.iters_run),
                                   float(r.wall_time)))
+
+    if solver is not None:
+        for i, target in mine:
+            record(i, solver(target, focus_kernels, defocus_kernels, cfg))
+    else:
+        # device loop of clip i+1 overlaps the host tail (shot count, records) of clip i
+        from concurrent.futures import ThreadPoolExecutor
+        from .optimizer import _assemble, _optimize_device
+        with ThreadPoolExecutor(max_workers=1) as pool:
+            pending = None
+            for i, target in mine:
+                parts = _optimize_device(target, focus_kernels, defocus_kernels, cfg)
+                if pending is not None:
+                    record(pending[0], pending[1].result())
+                pending = (i, pool.submit(_assemble, parts, cfg))
+            if pending is not None:
+                record(pending[0], pending[1].result())
     if synchronize:
         synchronize()
     seconds = max_over_ranks(time.perf_counter() - t0, group)
