@@ -135,6 +135,9 @@ typedef struct {
    * 1: modulation_search's phi - (dt*v_total)*|grad phi| (optimizer.py:328-331).
    * The two orders round differently; each mode reproduces its caller. */
   int update_form;
+  /* 1: skip the uniform-target check (a strip of a larger tile may be uniform;
+   * the caller checks the whole tile, optimizer.py:197-201) */
+  int skip_target_check;
 } lsopc_config;
 
 typedef struct {
@@ -172,6 +175,25 @@ int lsopc_session_destroy(lsopc_session* s);
 int lsopc_session_phi(lsopc_session* s, double* phi_dev);
 /* Number of kernel launches one DSO iteration enqueues (bench accounting). */
 int lsopc_session_launches_per_iter(const lsopc_session* s);
+
+/* Oversized tile split across ranks into full-height strips (BASELINE
+ * configs[4]).  The session's grid is this rank's window: its
+ * interior columns [ix0, ix1) plus halo columns refreshed from the
+ * neighbouring ranks each iteration; [xlo, xhi) bounds the x-neighbours of
+ * the phi stencil (replicate padding at the global tile edge).  After
+ * set_tile the iteration is driven phase by phase: each phase leaves this
+ * rank's partial scalars in lsopc_session_scalars() (8 doubles on the
+ * device: [0..1] losses (sum), [2..3] Polak-Ribiere dots (sum), [4..5]
+ * max |v_total|, max |grad phi| (max), [6] max step (max)), which the caller
+ * combines across ranks before the next phase; after phase 4 the caller
+ * refreshes the halo columns of lsopc_session_phi_ptr().  Forward phases
+ * threshold phi directly, so only phi needs exchanging. */
+int lsopc_session_set_tile(lsopc_session* s, int ix0, int ix1, int xlo, int xhi);
+int lsopc_session_phase(lsopc_session* s, int phase);
+double* lsopc_session_scalars(lsopc_session* s);
+double* lsopc_session_phi_ptr(lsopc_session* s);
+/* device pointer to the session's stop flag (int; non-zero once the stop rule fired) */
+int* lsopc_session_state_flag(lsopc_session* s);
 
 /* Measurement hook: run `reps` more iterations of the session, recording CUDA
  * events on the session stream at the pass boundaries, and write the mean

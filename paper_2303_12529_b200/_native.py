@@ -35,7 +35,8 @@ class LsopcConfig(ctypes.Structure):
                 ("d_upper", ctypes.c_double), ("d_lower", ctypes.c_double),
                 ("max_iters", ctypes.c_int), ("stop_rel_tol", ctypes.c_double),
                 ("stop_patience", ctypes.c_int), ("use_curvature", ctypes.c_int),
-                ("cg_restart_every", ctypes.c_int), ("update_form", ctypes.c_int)]
+                ("cg_restart_every", ctypes.c_int), ("update_form", ctypes.c_int),
+                ("skip_target_check", ctypes.c_int)]
 
 
 class LsopcResult(ctypes.Structure):
@@ -77,6 +78,11 @@ _SIGS = {
     "lsopc_session_launches_per_iter": (_I, [_P]),
     "lsopc_fracture": (_I, [_I, _I, _P, _P, _Z, ctypes.POINTER(_Z)]),
     "lsopc_session_time_passes": (_I, [_P, _I, ctypes.POINTER(_D)]),
+    "lsopc_session_set_tile": (_I, [_P, _I, _I, _I, _I]),
+    "lsopc_session_phase": (_I, [_P, _I]),
+    "lsopc_session_scalars": (_P, [_P]),
+    "lsopc_session_phi_ptr": (_P, [_P]),
+    "lsopc_session_state_flag": (_P, [_P]),
 }
 
 _lib = None

@@ -17,6 +17,16 @@ struct DevState {
   int it;  // index of the iteration in flight (advanced by the update's control kernel)
 };
 
+// Column ranges (window coordinates) of a strip of an oversized tile run on
+// one rank: [ix0, ix1) is the interior this rank owns (losses, dots, maxima,
+// updates), [xlo, xhi) bounds the x-neighbours of the phi stencil (replicate
+// padding at the global tile edge, halo data elsewhere).  The default covers
+// the whole grid.
+struct Tile {
+  int ix0, ix1, xlo, xhi;
+};
+inline Tile full_tile(int W) { return Tile{0, W, 0, W}; }
+
 struct LoopCfg {
   double alpha, beta, stop_rel_tol;
   int stop_patience;
@@ -32,9 +42,11 @@ void launch_curvature(int H, int W, const double* phi, const double* m, double w
                       cudaStream_t s);
 void launch_ls_velocity(int H, int W, const double* phi, const double* v, const double* dprev, const double* m,
                         double weight, int use_curv, const DevState* st, double* d, double* u, double* gm,
-                        double* partials, cudaStream_t s);
-void launch_ls_update(size_t n, double* phi, const double* u, const double* gm, double lo, double hi,
-                      const DevState* st, uint8_t* mask, double* partials, cudaStream_t s);
+                        double* partials, Tile t, cudaStream_t s);
+void launch_ls_update(int H, int W, double* phi, const double* u, const double* gm, double lo, double hi,
+                      const DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s);
+// fixed-order reduction of nb blocks of nv partials (sum or max) into out[0..nv)
+void launch_reduce_partials(const double* part, int nb, int nv, int is_max, double* out, cudaStream_t s);
 void launch_copy_best(size_t n, const double* phi, double* best, const DevState* st, cudaStream_t s);
 void launch_after_forward(const double* part, int nb, LoopCfg c, DevState* st, double* hist, cudaStream_t s);
 // restart_every: Polak-Ribiere restart period (optimizer.py:253); iteration 0 always restarts
@@ -43,9 +55,9 @@ void launch_after_velocity(const double* part, int nb, double eta, DevState* st,
 void launch_after_update(const double* part, int nb, DevState* st, double* hist, cudaStream_t s);
 void launch_elementwise(int op, size_t n, const double* a, const double* b, double p0, double p1, double p2,
                         double* out, uint8_t* out8, cudaStream_t s);
-// out: device scalar
+// out: device scalar.  W > 0 restricts RD_COUNTNEQ8 to columns [ix0, ix1) of rows of width W.
 void launch_reduce(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
-                   double* partials, double* out, cudaStream_t s);
+                   double* partials, double* out, cudaStream_t s, int W = 0, int ix0 = 0, int ix1 = 0);
 
 // exact EDT -> truncated signed distance (levelset.py:86-101)
 void launch_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_lower, double* phi,

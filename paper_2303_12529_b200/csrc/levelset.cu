@@ -65,9 +65,11 @@ struct Geom {
   double gx, gy, gxx, gyy, gxy;
 };
 
-// levelset.py:112-118, replicate ("edge") padding
-LS_D Geom geometry_at(const double* __restrict__ phi, int H, int W, int y, int x) {
-  const int xe = x + 1 < W ? x + 1 : W - 1, xw = x > 0 ? x - 1 : 0;
+// levelset.py:112-118, replicate ("edge") padding; x-neighbours clamped to
+// [xlo, xhi) (the whole row unless the grid is a strip of a larger tile)
+LS_D Geom geometry_at(const double* __restrict__ phi, int H, int W, int y, int x, int xlo = 0, int xhi = -1) {
+  if (xhi < 0) xhi = W;
+  const int xe = x + 1 < xhi ? x + 1 : xhi - 1, xw = x > xlo ? x - 1 : xlo;
   const int ys = y + 1 < H ? y + 1 : H - 1, yn = y > 0 ? y - 1 : 0;
   const double* r = phi + (size_t)y * W;
   const double* rs = phi + (size_t)ys * W;
@@ -122,7 +124,7 @@ k_curvature(int H, int W, const double* __restrict__ phi, const double* __restri
 __global__ void __launch_bounds__(kThreads)
 k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __restrict__ v,
               const double* __restrict__ dprev, const double* __restrict__ m, double weight, int use_curv,
-              const DevState* st, double* d_out, double* u_out, double* gm_out, double* partials) {
+              const DevState* st, double* d_out, double* u_out, double* gm_out, double* partials, Tile tl) {
   __shared__ double red[64];
   if (st->stopped) return;
   const int use_beta = st->use_beta;
@@ -131,7 +133,7 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
   double mx[2] = {0.0, 0.0};  // max |v_total|, max |grad phi|
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     int y = (int)(i / W), x = (int)(i % W);
-    Geom g = geometry_at(phi, H, W, y, x);
+    Geom g = geometry_at(phi, H, W, y, x, tl.xlo, tl.xhi);
     double gm = np_hypot(g.gx, g.gy);
     double d = -v[i];
     if (use_beta) d = add(d, mul(beta, dprev[i]));
@@ -148,8 +150,10 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
     } else {
       u_out[i] = mul(-vt, gm);
     }
-    mx[0] = fmax(mx[0], fabs(vt));
-    mx[1] = fmax(mx[1], gm);
+    if (x >= tl.ix0 && x < tl.ix1) {
+      mx[0] = fmax(mx[0], fabs(vt));
+      mx[1] = fmax(mx[1], gm);
+    }
   }
   block_max<2>(mx, red);
   if (threadIdx.x == 0) {
@@ -160,13 +164,16 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
 
 // optimizer.py:266-268: phi <- clip(phi + dt * u, D_l, D_u); next mask = [phi <= 0]
 __global__ void __launch_bounds__(kThreads)
-k_ls_update(size_t n, double* phi, const double* __restrict__ u, const double* __restrict__ gm, double lo,
-            double hi, const DevState* st, uint8_t* mask, double* partials) {
+k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const double* __restrict__ gm, double lo,
+            double hi, const DevState* st, uint8_t* mask, double* partials, Tile tl) {
   __shared__ double red[32];
   if (st->stopped) return;
   const double dt = st->dt;
+  const size_t n = (size_t)H * W;
   double mx[1] = {0.0};
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % W);
+    if (x < tl.ix0 || x >= tl.ix1) continue;  // strip halo: owned by a neighbour rank
     double step, p;
     if (gm) {  // optimizer.py:329: phi - dt * v_total * grad_mag
       step = mul(mul(dt, u[i]), gm[i]);
@@ -317,7 +324,7 @@ __global__ void k_elementwise(int op, size_t n, const double* __restrict__ a, co
 
 __global__ void __launch_bounds__(kThreads)
 k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restrict__ b,
-         const uint8_t* __restrict__ a8, const uint8_t* __restrict__ b8, double* partials) {
+         const uint8_t* __restrict__ a8, const uint8_t* __restrict__ b8, double* partials, int W, int ix0, int ix1) {
   __shared__ double red[32];
   double acc[1] = {0.0};
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -326,7 +333,10 @@ k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restric
       case RD_DOT: acc[0] += a[i] * b[i]; break;
       case RD_DOTDIFF: acc[0] += a[i] * (a[i] - b[i]); break;
       case RD_MAXABS: acc[0] = fmax(acc[0], fabs(a[i])); break;
-      case RD_COUNTNEQ8: acc[0] += (a8[i] != (b8 ? b8[i] : 0)) ? 1.0 : 0.0; break;  // b8 null: vs 0
+      case RD_COUNTNEQ8:  // b8 null: vs 0; W > 0: columns [ix0, ix1) only
+        if (W > 0 && ((int)(i % W) < ix0 || (int)(i % W) >= ix1)) break;
+        acc[0] += (a8[i] != (b8 ? b8[i] : 0)) ? 1.0 : 0.0;
+        break;
       case RD_COUNTNEQ: acc[0] += (a[i] != b[i]) ? 1.0 : 0.0; break;
       case RD_NONFINITE: if (!isfinite(a[i])) acc[0] = fmax(acc[0], (double)(n - i)); break;
       default: break;
@@ -335,6 +345,15 @@ k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restric
   if (op == RD_MAXABS || op == RD_NONFINITE) block_max<1>(acc, red);
   else block_sum<1>(acc, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
+}
+
+template <int NV, bool MAX>
+__global__ void k_reduce_partials(const double* part, int nb, double* out) {
+  __shared__ double red[64];
+  double r[NV];
+  reduce_partials<NV, MAX>(part, nb, r, red);
+  if (threadIdx.x == 0)
+    for (int j = 0; j < NV; ++j) out[j] = r[j];
 }
 
 __global__ void k_reduce_final(int op, const double* part, int nb, double* out) {
@@ -359,12 +378,12 @@ void launch_curvature(int H, int W, const double* phi, const double* m, double w
 }
 void launch_ls_velocity(int H, int W, const double* phi, const double* v, const double* dprev, const double* m,
                         double weight, int use_curv, const DevState* st, double* d, double* u, double* gm,
-                        double* partials, cudaStream_t s) {
-  k_ls_velocity<<<kBlocks, kThreads, 0, s>>>(H, W, phi, v, dprev, m, weight, use_curv, st, d, u, gm, partials);
+                        double* partials, Tile t, cudaStream_t s) {
+  k_ls_velocity<<<kBlocks, kThreads, 0, s>>>(H, W, phi, v, dprev, m, weight, use_curv, st, d, u, gm, partials, t);
 }
-void launch_ls_update(size_t n, double* phi, const double* u, const double* gm, double lo, double hi,
-                      const DevState* st, uint8_t* mask, double* partials, cudaStream_t s) {
-  k_ls_update<<<kBlocks, kThreads, 0, s>>>(n, phi, u, gm, lo, hi, st, mask, partials);
+void launch_ls_update(int H, int W, double* phi, const double* u, const double* gm, double lo, double hi,
+                      const DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s) {
+  k_ls_update<<<kBlocks, kThreads, 0, s>>>(H, W, phi, u, gm, lo, hi, st, mask, partials, t);
 }
 void launch_copy_best(size_t n, const double* phi, double* best, const DevState* st, cudaStream_t s) {
   k_copy_best<<<kBlocks, kThreads, 0, s>>>(n, phi, best, st);
@@ -381,13 +400,22 @@ void launch_after_velocity(const double* part, int nb, double eta, DevState* st,
 void launch_after_update(const double* part, int nb, DevState* st, double* hist, cudaStream_t s) {
   k_after_update<<<1, 256, 0, s>>>(part, nb, st, hist);
 }
+void launch_reduce_partials(const double* part, int nb, int nv, int is_max, double* out, cudaStream_t s) {
+  if (nv == 1) {
+    if (is_max) k_reduce_partials<1, true><<<1, 256, 0, s>>>(part, nb, out);
+    else k_reduce_partials<1, false><<<1, 256, 0, s>>>(part, nb, out);
+  } else {
+    if (is_max) k_reduce_partials<2, true><<<1, 256, 0, s>>>(part, nb, out);
+    else k_reduce_partials<2, false><<<1, 256, 0, s>>>(part, nb, out);
+  }
+}
 void launch_elementwise(int op, size_t n, const double* a, const double* b, double p0, double p1, double p2,
                         double* out, uint8_t* out8, cudaStream_t s) {
   k_elementwise<<<kBlocks, kThreads, 0, s>>>(op, n, a, b, p0, p1, p2, out, out8);
 }
 void launch_reduce(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
-                   double* partials, double* out, cudaStream_t s) {
-  k_reduce<<<kBlocks, kThreads, 0, s>>>(op, n, a, b, a8, b8, partials);
+                   double* partials, double* out, cudaStream_t s, int W, int ix0, int ix1) {
+  k_reduce<<<kBlocks, kThreads, 0, s>>>(op, n, a, b, a8, b8, partials, W, ix0, ix1);
   k_reduce_final<<<1, 256, 0, s>>>(op, partials, kBlocks, out);
 }
 

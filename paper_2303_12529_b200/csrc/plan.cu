@@ -111,7 +111,7 @@ void check_kset(const lsopc_plan* p, const lsopc_kset* k) {
 }
 
 double reduce_to_host(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
-                      lsopc_plan* plan, cudaStream_t s) {
+                      lsopc_plan* plan, cudaStream_t s, int W = 0, int ix0 = 0, int ix1 = 0) {
   DevBuf tmp;
   double* part;
   double* out;
@@ -123,7 +123,7 @@ double reduce_to_host(int op, size_t n, const double* a, const double* b, const 
     part = tmp.as<double>();
     out = part + ls_blocks();
   }
-  launch_reduce(op, n, a, b, a8, b8, part, out, s);
+  launch_reduce(op, n, a, b, a8, b8, part, out, s, W, ix0, ix1);
   ck_launch("reduce");
   double h = 0.0;
   ck(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, s), "memcpy");
@@ -424,6 +424,10 @@ struct lsopc_session {
   DevBuf target, phi, best, v[2], d[2], u, mask, mod, hist, state, part_ls, part_up, dots, gm;
   int it = 0;  // iterations enqueued
   bool have_mod = false;
+  // strip of an oversized tile (lsopc_session_set_tile): interior / stencil columns
+  bool tiled = false;
+  Tile tile{};
+  DevBuf scalars;  // 8 doubles exchanged with the other ranks between phases
   // one DSO iteration captured as a CUDA graph per buffer parity (it & 1)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int* hflag = nullptr;  // pinned host copies of DevState::stopped (async polling)
@@ -435,7 +439,7 @@ struct lsopc_session {
       if (e) cudaEventDestroy(e);
     if (hflag) cudaFreeHost(hflag);
     for (DevBuf* b : {&target, &phi, &best, &v[0], &v[1], &d[0], &d[1], &u, &mask, &mod, &hist, &state, &part_ls,
-                      &part_up, &dots, &gm})
+                      &part_up, &dots, &gm, &scalars})
       b->release();
   }
   DevState* st() const { return state.as<DevState>(); }
@@ -540,14 +544,73 @@ void enqueue_iteration(lsopc_session* ss, int par, cudaStream_t s, cudaEvent_t* 
   // level-set step
   launch_ls_velocity(g.H, g.W, ss->phi.as<double>(), v, dprev, ss->have_mod ? ss->mod.as<double>() : nullptr,
                      c.curvature_weight, c.use_curvature, st, d, ss->u.as<double>(),
-                     c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), s);
+                     c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), full_tile(g.W), s);
   launch_after_velocity(ss->part_ls.as<double>(), ls_blocks(), c.eta, st, ss->hist.as<double>(), s);
-  launch_ls_update(n, ss->phi.as<double>(), ss->u.as<double>(), c.update_form ? ss->gm.as<double>() : nullptr,
+  launch_ls_update(g.H, g.W, ss->phi.as<double>(), ss->u.as<double>(), c.update_form ? ss->gm.as<double>() : nullptr,
                    c.d_lower, c.d_upper, st, ss->mask.as<uint8_t>(),
-                   ss->part_up.as<double>(), s);
+                   ss->part_up.as<double>(), full_tile(g.W), s);
   launch_after_update(ss->part_up.as<double>(), ls_blocks(), st, ss->hist.as<double>(), s);
   mark(8);
   ck_launch("dso iteration");
+}
+
+// One phase of a strip iteration (lsopc_session_phase).  Each phase ends
+// with this rank's partial scalars in ss->scalars; the caller combines them
+// across ranks (sum / max) before the next phase consumes them.
+void enqueue_phase(lsopc_session* ss, int phase, cudaStream_t s) {
+  lsopc_plan* p = ss->plan;
+  const Grid& g = p->g;
+  const size_t n = g.n();
+  DevState* st = ss->st();
+  StopFlag stop = &st->stopped;
+  const lsopc_config& c = ss->cfg;
+  const int par = ss->it & 1;
+  double* v = ss->v[par].as<double>();
+  double* vprev = ss->v[par ^ 1].as<double>();
+  double* d = ss->d[par].as<double>();
+  double* dprev = ss->d[par ^ 1].as<double>();
+  double* sc = ss->scalars.as<double>();
+  const Tile& t = ss->tile;
+  SpecSet sets[2] = {spec_set(p, ss->focus, 0, 0), spec_set(p, ss->defocus, 1, ss->focus->nk)};
+  switch (phase) {
+    case 0: {  // forward from phi (the halo columns were refreshed by the caller) -> sum losses
+      launch_mask_fft(g, nullptr, nullptr, ss->phi.as<double>(), p->mhat.p, p->scratch.p, stop, s);
+      launch_f1(g, p->mhat.p, sets, 2, stop, s);
+      launch_f2(g, sets, 2, nullptr, stop, s);
+      ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
+      launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr,
+                    nullptr, nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s, t.ix0, t.ix1);
+      launch_reduce_partials(p->partials.as<double>(), reduce_blocks(), 2, 0, sc, s);
+    } break;
+    case 1: {  // stop rule on the global losses; adjoint -> sum PR dots
+      LoopCfg lc{c.alpha, c.beta, c.stop_rel_tol, c.stop_patience};
+      launch_after_forward(sc, 1, lc, st, ss->hist.as<double>(), s);
+      launch_copy_best(n, ss->phi.as<double>(), ss->best.as<double>(), st, s);
+      launch_a1(g, sets, 2, stop, s);
+      launch_a2(g, sets, 2, stop, s);
+      const int nd = launch_adjoint_finish(g, p->V0.p, p->V1.p, 4.0 * c.sigma_z / (double)n, v, vprev,
+                                           ss->dots.as<double>(), stop, s, t.ix0, t.ix1);
+      launch_reduce_partials(ss->dots.as<double>(), nd, 2, 0, sc + 2, s);
+    } break;
+    case 2: {  // CG on the global dots; level-set velocity -> max |v_total|, max |grad phi|
+      launch_after_grad(sc + 2, 1, c.cg_restart_every, st, s);
+      launch_ls_velocity(g.H, g.W, ss->phi.as<double>(), v, dprev, ss->have_mod ? ss->mod.as<double>() : nullptr,
+                         c.curvature_weight, c.use_curvature, st, d, ss->u.as<double>(),
+                         c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), t, s);
+      launch_reduce_partials(ss->part_ls.as<double>(), ls_blocks(), 2, 1, sc + 4, s);
+    } break;
+    case 3: {  // CFL step on the global max; interior update -> max step
+      launch_after_velocity(sc + 4, 1, c.eta, st, ss->hist.as<double>(), s);
+      launch_ls_update(g.H, g.W, ss->phi.as<double>(), ss->u.as<double>(),
+                       c.update_form ? ss->gm.as<double>() : nullptr, c.d_lower, c.d_upper, st,
+                       ss->mask.as<uint8_t>(), ss->part_up.as<double>(), t, s);
+      launch_reduce_partials(ss->part_up.as<double>(), ls_blocks(), 1, 1, sc + 6, s);
+    } break;
+    default:  // record on the global max step
+      launch_after_update(sc + 6, 1, st, ss->hist.as<double>(), s);
+      break;
+  }
+  ck_launch("dso phase");
 }
 
 }  // namespace
@@ -599,7 +662,7 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
       }
       ck(cudaMemcpyAsync(ss->target.p, target_dev, n, cudaMemcpyDeviceToDevice, s), "memcpy");
       // optimizer.py:197-201: uniform target -> DegenerateInputError
-      {
+      if (!cfg->skip_target_check) {
         double lit = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, ss->target.as<uint8_t>(), nullptr, plan, s);
         if (lit == 0.0 || lit == (double)n) throw Error(LSOPC_EDEGENERATE, "target layout is uniform");
       }
@@ -696,8 +759,11 @@ int lsopc_session_finish(lsopc_session* ss, double* best_phi_dev, uint8_t* final
     launch_resist(g, p->If.p, p->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr, nullptr, hn, hn + n,
                   hn + 2 * n, nullptr, nullptr, s);
     ck_launch("final prints");
-    double l2 = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn, ss->target.as<uint8_t>(), p, s);
-    double pvb = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn + n, hn + 2 * n, p, s);
+    const int cw = ss->tiled ? g.W : 0;  // strip: count the interior columns only
+    double l2 = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn, ss->target.as<uint8_t>(), p, s, cw,
+                               ss->tile.ix0, ss->tile.ix1);
+    double pvb = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn + n, hn + 2 * n, p, s, cw, ss->tile.ix0,
+                                ss->tile.ix1);
     if (best_phi_dev) ck(cudaMemcpyAsync(best_phi_dev, ss->best.p, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
     ck(cudaStreamSynchronize(s), "sync");
     if (res) {
@@ -723,6 +789,34 @@ int lsopc_session_destroy(lsopc_session* ss) {
     give_to_pool(ss);
   });
 }
+
+int lsopc_session_set_tile(lsopc_session* ss, int ix0, int ix1, int xlo, int xhi) {
+  return guarded([&] {
+    if (!ss) throw Error(LSOPC_EINVAL, "null session");
+    const int W = ss->plan->g.W;
+    if (!(0 <= ix0 && ix0 < ix1 && ix1 <= W && 0 <= xlo && xlo <= ix0 && ix1 <= xhi && xhi <= W))
+      throw Error(LSOPC_EINVAL, "bad strip geometry");
+    if (ss->it) throw Error(LSOPC_EINVAL, "set the strip before the first iteration");
+    ss->tiled = true;
+    ss->tile = Tile{ix0, ix1, xlo, xhi};
+    ss->scalars.ensure(8 * sizeof(double));
+    ck(cudaMemsetAsync(ss->scalars.p, 0, 8 * sizeof(double), ss->s), "memset");
+  });
+}
+
+int lsopc_session_phase(lsopc_session* ss, int phase) {
+  return guarded([&] {
+    if (!ss || !ss->tiled) throw Error(LSOPC_EINVAL, "phases need a strip session (lsopc_session_set_tile)");
+    if (phase < 0 || phase > 4) throw Error(LSOPC_EINVAL, "phase must be 0..4");
+    if (phase == 0 && ss->it >= ss->cfg.max_iters) throw Error(LSOPC_EINVAL, "max_iters reached");
+    enqueue_phase(ss, phase, ss->s);
+    if (phase == 4) ++ss->it;
+  });
+}
+
+double* lsopc_session_scalars(lsopc_session* ss) { return ss ? ss->scalars.as<double>() : nullptr; }
+double* lsopc_session_phi_ptr(lsopc_session* ss) { return ss ? ss->phi.as<double>() : nullptr; }
+int* lsopc_session_state_flag(lsopc_session* ss) { return ss ? &ss->st()->stopped : nullptr; }
 
 int lsopc_session_time_passes(lsopc_session* ss, int reps, double* ms_out) {
   return guarded([&] {

@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(kRedThreads)
 k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uint8_t* __restrict__ tu8,
          const double* __restrict__ tf, ResistParams p, R* wf, R* wd, double* z_nom, double* z_in,
          double* z_out, uint8_t* h_nom, uint8_t* h_in, uint8_t* h_out, double* partials,
-         StopFlag stop) {
+         StopFlag stop, int W, int ix0, int ix1) {
   __shared__ double red[64];
   if (stop && *stop) return;
   double acc[2] = {0.0, 0.0};
@@ -52,8 +52,11 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
     if (have_t) {
       double zt = tu8 ? (double)tu8[i] : tf[i];
       double dn = zn - zt, di = zi - zt, dout = zo - zt;
-      acc[0] += dn * dn;               // optimizer.py:88-90
-      acc[1] += di * di + dout * dout;  // optimizer.py:93-96
+      const int x = (int)(i % W);
+      if (x >= ix0 && x < ix1) {         // strip interior (the whole row by default)
+        acc[0] += dn * dn;               // optimizer.py:88-90
+        acc[1] += di * di + dout * dout;  // optimizer.py:93-96
+      }
       if (wf) {
         // optimizer.py:109 gate, 114-134 doses and alpha/beta folded per kernel set
         double gn = dn * zn * (1.0 - zn);
@@ -95,15 +98,18 @@ int reduce_blocks() { return kRedBlocks; }
 void launch_resist(const Grid& g, const void* If, const void* Id, const uint8_t* tu8, const double* tf,
                    ResistParams p, void* wf, void* wd, double* z_nom, double* z_in, double* z_out,
                    uint8_t* h_nom, uint8_t* h_in, uint8_t* h_out, double* partials, StopFlag stop,
-                   cudaStream_t s) {
+                   cudaStream_t s, int ix0, int ix1) {
+  if (ix1 <= 0) ix1 = g.W;
   if (g.prec == F64)
     k_resist<double><<<kRedBlocks, kRedThreads, 0, s>>>(
         g.n(), static_cast<const double*>(If), static_cast<const double*>(Id), tu8, tf, p,
-        static_cast<double*>(wf), static_cast<double*>(wd), z_nom, z_in, z_out, h_nom, h_in, h_out, partials, stop);
+        static_cast<double*>(wf), static_cast<double*>(wd), z_nom, z_in, z_out, h_nom, h_in, h_out, partials, stop,
+        g.W, ix0, ix1);
   else
     k_resist<float><<<kRedBlocks, kRedThreads, 0, s>>>(
         g.n(), static_cast<const float*>(If), static_cast<const float*>(Id), tu8, tf, p,
-        static_cast<float*>(wf), static_cast<float*>(wd), z_nom, z_in, z_out, h_nom, h_in, h_out, partials, stop);
+        static_cast<float*>(wf), static_cast<float*>(wd), z_nom, z_in, z_out, h_nom, h_in, h_out, partials, stop,
+        g.W, ix0, ix1);
 }
 
 void launch_scale_intensity(const Grid& g, const void* I, double dose, double* out, cudaStream_t s) {

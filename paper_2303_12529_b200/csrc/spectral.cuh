@@ -599,6 +599,7 @@ template <typename R> struct A3Op : OpBase {
   double* out;
   const double* vp;
   double* dots;
+  int ix0, ix1;  // dots over columns [ix0, ix1)
   LS_D void prefetch(int it, int, C* b, C*) const {
     eng::gather_rect<sizeof(C)>(b, V0, sh.ct(), it << sh.lgR, sh.lgR, 0, sh.lgW);
   }
@@ -610,7 +611,7 @@ template <typename R> struct A3Op : OpBase {
     double* out;
     const double* vp;
     State& S;
-    int y0, lgn, W;
+    int y0, lgn, W, ix0, ix1;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const C x = b[nat_row<LGN, ST>(seq, j, r, lgn)];
       return v1 ? x + __ldg(&v1[ct_row<LGN, ST, C>(L, y0 + seq, j, r)]) : x;
@@ -619,7 +620,8 @@ template <typename R> struct A3Op : OpBase {
       const size_t p = rm_row<LGN, ST>(W, y0 + seq, j, r);
       const double val = scale * (double)v.x;
       out[p] = val;
-      if (vp) {
+      const int x = j + r * ST;
+      if (vp && x >= ix0 && x < ix1) {
         const double q = vp[p];
         S.acc[0] += val * (val - q);
         S.acc[1] += q * q;
@@ -630,7 +632,7 @@ template <typename R> struct A3Op : OpBase {
     const Geo g = sh.grow();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      F<LGN> f{b, V1, sh.ct(), scale, out, vp, S, it << sh.lgR, sh.lgW, sh.W};
+      F<LGN> f{b, V1, sh.ct(), scale, out, vp, S, it << sh.lgR, sh.lgW, sh.W, ix0, ix1};
       eng::run_fix<LGN, false, true>(g, b, tw, f);
     });
   }
@@ -1245,7 +1247,7 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
 
 template <typename R>
 int finish_impl(const Grid& g, const void* V0, const void* V1, double scale, double* out, const double* vp,
-                double* dots, StopFlag stop, cudaStream_t s) {
+                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1) {
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   A3Op<R> a3;
@@ -1257,6 +1259,8 @@ int finish_impl(const Grid& g, const void* V0, const void* V1, double scale, dou
   a3.out = out;
   a3.vp = vp;
   a3.dots = dots;
+  a3.ix0 = ix0;
+  a3.ix1 = ix1 > 0 ? ix1 : g.W;
   a3.bufE = row_bufE(sh);
   a3.nitems = g.H >> sh.lgR;
   int grid = launch_op<R>(a3, row_threads(sh), 0, stop, s, finish_max_blocks());

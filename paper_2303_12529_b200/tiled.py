@@ -1,0 +1,259 @@
+"""Oversized tile split across ranks (BASELINE configs[4]).
+
+The reference optimises one periodic N x N tile with circular FFTs
+(`fields.py:5-6`, `litho.py:114-126`).  Here the tile is cut into full-height
+strips, one per rank.  Each rank runs the unchanged device pipeline on a
+power-of-two window that holds its interior columns plus halos of at least
+HALO = 2 * (K // 2) columns on each side (the forward field at a pixel needs
+the mask within +-K//2, the adjoint within +-2 * (K//2)), so every interior
+value equals the full-tile computation.  Per iteration:
+
+    phase 0  forward on the window                -> all_reduce(sum)  losses
+    phase 1  stop rule, adjoint, CG dot partials  -> all_reduce(sum)  dots
+    phase 2  CG direction, level-set velocity     -> all_reduce(max)  |v|, |grad phi|
+    phase 3  CFL step, interior update            -> all_reduce(max)  step
+    phase 4  history record
+    halo     exchange HALO columns of phi with both neighbours (wrapping)
+
+Optics wrap around the tile edge (periodic, like the reference's FFT); the
+phi stencil uses replicate padding at the global left/right edge
+(`levelset.py:112`), so the edge ranks clamp their stencil to the interior.
+Losses, dots, maxima and the final L2/PVB are summed over interiors only.
+All ranks see the same scalars, so the stop rule, best iterate and CG
+restarts agree everywhere.
+
+Collectives go through `torch.distributed` on the default group: NCCL keeps
+them on the stream; with gloo (CPU tests, several ranks sharing one GPU) the
+small buffers are staged through host memory.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nv
+from . import litho
+from .levelset import LevelSetField
+from .metrics import MetricsReport, shot_count
+
+
+@dataclass
+class Strip:
+    """Geometry of one rank's strip: interior [x0, x1) of the global tile,
+    window width ww whose column c is global column (x0 - hl + c) mod W."""
+    rank: int
+    world: int
+    H: int
+    W: int
+    x0: int
+    x1: int
+    ww: int
+    hl: int
+    halo: int
+
+    @property
+    def interior(self):
+        return self.hl, self.hl + (self.x1 - self.x0)
+
+    def columns(self):
+        """Global column of every window column."""
+        return (self.x0 - self.hl + np.arange(self.ww)) % self.W
+
+    def stencil_bounds(self):
+        """x-neighbour clamp of the phi stencil in window coordinates."""
+        i0, i1 = self.interior
+        return (i0 if self.rank == 0 else 0), (i1 if self.rank == self.world - 1 else self.ww)
+
+
+def strip_geometry(H, W, world, rank, K):
+    """Full-height strips of equal width; windows are powers of two."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world size {world}")
+    if W % world:
+        raise ValueError(f"tile width {W} is not divisible by {world} ranks")
+    halo = 2 * (K // 2)
+    wi = W // world
+    x0 = rank * wi
+    if world == 1:
+        return Strip(rank, world, H, W, 0, W, W, 0, halo)
+    if halo > wi:
+        raise ValueError(f"strip width {wi} is narrower than the halo {halo}")
+    if wi + 2 * halo > W:
+        raise ValueError(f"{world} strips of a {W}-wide tile cannot carry {halo}-column halos")
+    ww = 1
+    while ww < wi + 2 * halo:
+        ww *= 2
+    ww = min(ww, W)  # at most the whole tile (then the window wraps onto itself)
+    hl = (ww - wi) // 2
+    return Strip(rank, world, H, W, x0, x0 + wi, ww, hl, halo)
+
+
+class _CudaView:
+    """Zero-copy torch view of a device pointer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def _backend_is_nccl():
+    dist = _dist()
+    return dist.is_initialized() and dist.get_backend() == "nccl"
+
+
+def all_reduce_(t, op):
+    """In-place all-reduce of a small device tensor (staged on the host for gloo)."""
+    dist = _dist()
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return t
+    if _backend_is_nccl():
+        dist.all_reduce(t, op=op)
+    else:
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    return t
+
+
+def exchange_halos(phi, strip):
+    """Refresh the HALO columns on each side of the interior of `phi`
+    (H x ww torch tensor) from the neighbouring ranks' interiors (wrapping)."""
+    dist = _dist()
+    if strip.world == 1:
+        return
+    import torch
+    h = strip.halo
+    i0, i1 = strip.interior
+    left, right = (strip.rank - 1) % strip.world, (strip.rank + 1) % strip.world
+    nccl = _backend_is_nccl()
+    stage = (lambda t: t) if nccl else (lambda t: t.cpu())
+    send_l = stage(phi[:, i0:i0 + h].contiguous())    # -> left neighbour's right halo
+    send_r = stage(phi[:, i1 - h:i1].contiguous())    # -> right neighbour's left halo
+    recv_l = torch.empty_like(send_l)
+    recv_r = torch.empty_like(send_r)
+    # tags keep the two messages apart when left == right (two ranks)
+    ops = [dist.P2POp(dist.isend, send_l, left, tag=1), dist.P2POp(dist.isend, send_r, right, tag=2),
+           dist.P2POp(dist.irecv, recv_l, left, tag=2), dist.P2POp(dist.irecv, recv_r, right, tag=1)]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    phi[:, i0 - h:i0].copy_(recv_l)
+    phi[:, i1:i1 + h].copy_(recv_r)
+
+
+@dataclass
+class TiledResult:
+    final_mask: np.ndarray      # global tile (every rank)
+    final_phi: LevelSetField    # global tile (every rank)
+    metrics: MetricsReport
+    loss_history: list
+    iters_run: int
+    wall_time: float
+
+
+def optimize_tiled(target, focus_kernels, defocus_kernels, cfg, phi0=None):
+    """`optimize` (optimizer.py:204-284) of one tile split into strips over
+    the ranks of the default process group (a single process runs the whole
+    tile as one strip).  Every rank passes the same global `target` (and
+    `phi0`); every rank returns the assembled global result."""
+    import time
+    import torch
+    from .optimizer import IterationRecord, _check_target, _native_cfg
+
+    t0 = time.perf_counter()
+    dist = _dist()
+    rank, world = (dist.get_rank(), dist.get_world_size()) if dist.is_initialized() else (0, 1)
+    target = _check_target(target)
+    H, W = target.shape
+    st = strip_geometry(H, W, world, rank, focus_kernels.side)
+    cols = st.columns()
+    i0, i1 = st.interior
+    xlo, xhi = st.stencil_bounds()
+    prec = cfg.precision
+
+    # initial level set: the whole tile's TSDF (levelset.py:86-101) or phi0, windowed
+    if phi0 is None:
+        td_full = nv.to_dev(target, np.uint8)
+        phi_full = nv.empty((H, W), np.float64)
+        nv.check(nv.lib().lsopc_tsdf(H, W, nv.ptr(td_full), float(cfg.d_upper), float(cfg.d_lower),
+                                     nv.ptr(phi_full), nv.stream()))
+        phi_win = phi_full[:, torch.as_tensor(cols, device=phi_full.device)].contiguous()
+        del phi_full, td_full
+    else:
+        p = np.asarray(phi0.phi, dtype=np.float64)
+        if p.shape != target.shape:
+            raise ValueError("phi0 dimensions do not match target")
+        phi_win = nv.to_dev(np.ascontiguousarray(p[:, cols]))
+    tgt_win = nv.to_dev(np.ascontiguousarray(target[:, cols]), np.uint8)
+
+    fk = litho.device_kernels(focus_kernels, (H, st.ww), prec)
+    dk = litho.device_kernels(defocus_kernels, (H, st.ww), prec)
+    c = _native_cfg(cfg)
+    c.skip_target_check = 1
+    L = nv.lib()
+    sess = ctypes.c_void_p()
+    nv.check(L.lsopc_session_create(fk.plan.handle, fk.handle, dk.handle, nv.ptr(tgt_win), nv.ptr(phi_win), None,
+                                    ctypes.byref(c), nv.stream(), ctypes.byref(sess)))
+    try:
+        nv.check(L.lsopc_session_set_tile(sess, i0, i1, xlo, xhi))
+        sc = torch.as_tensor(_CudaView(L.lsopc_session_scalars(sess), (8,), "<f8"), device="cuda")
+        phi = torch.as_tensor(_CudaView(L.lsopc_session_phi_ptr(sess), (H, st.ww), "<f8"), device="cuda")
+        flag = torch.as_tensor(_CudaView(L.lsopc_session_state_flag(sess), (1,), "<i4"), device="cuda")
+        SUM, MAX = dist.ReduceOp.SUM, dist.ReduceOp.MAX
+        for _ in range(cfg.max_iters):
+            nv.check(L.lsopc_session_phase(sess, 0))
+            all_reduce_(sc[0:2], SUM)
+            nv.check(L.lsopc_session_phase(sess, 1))
+            all_reduce_(sc[2:4], SUM)
+            nv.check(L.lsopc_session_phase(sess, 2))
+            all_reduce_(sc[4:6], MAX)
+            nv.check(L.lsopc_session_phase(sess, 3))
+            all_reduce_(sc[6:7], MAX)
+            nv.check(L.lsopc_session_phase(sess, 4))
+            if int(flag.item()):   # identical on every rank (same global scalars)
+                break
+            exchange_halos(phi, st)
+        best = nv.empty((H, st.ww), np.float64)
+        fmask = nv.empty((H, st.ww), np.uint8)
+        hist = np.zeros((cfg.max_iters + 1, 7))
+        res = nv.LsopcResult()
+        nv.check(L.lsopc_session_finish(sess, nv.ptr(best), nv.ptr(fmask), hist.ctypes.data_as(ctypes.c_void_p),
+                                        ctypes.byref(res)))
+    finally:
+        L.lsopc_session_destroy(sess)
+    counts = torch.tensor([float(res.l2), float(res.pvband)], dtype=torch.float64, device="cuda")
+    all_reduce_(counts, dist.ReduceOp.SUM)
+    # assemble the global mask and phi from every rank's interior
+    my_mask = fmask[:, i0:i1].contiguous()
+    my_phi = best[:, i0:i1].contiguous()
+    if world > 1:
+        if _backend_is_nccl():
+            masks = [torch.empty_like(my_mask) for _ in range(world)]
+            phis = [torch.empty_like(my_phi) for _ in range(world)]
+            dist.all_gather(masks, my_mask)
+            dist.all_gather(phis, my_phi)
+            masks = [m.cpu().numpy() for m in masks]
+            phis = [p.cpu().numpy() for p in phis]
+        else:
+            masks = [None] * world
+            phis = [None] * world
+            dist.all_gather_object(masks, my_mask.cpu().numpy())
+            dist.all_gather_object(phis, my_phi.cpu().numpy())
+        final_mask = np.concatenate(masks, axis=1)
+        final_phi = np.concatenate(phis, axis=1)
+    else:
+        final_mask = my_mask.cpu().numpy()
+        final_phi = my_phi.cpu().numpy()
+    wall = time.perf_counter() - t0
+    history = [IterationRecord(*(float(v) for v in row)) for row in hist[:res.iters]]
+    report = MetricsReport(l2=int(counts[0].item()), pvband=int(counts[1].item()), shots=shot_count(final_mask),
+                           wall_time=wall, iters=res.iters)
+    return TiledResult(final_mask=final_mask, final_phi=LevelSetField(final_phi, cfg.d_upper, cfg.d_lower),
+                       metrics=report, loss_history=history, iters_run=res.iters, wall_time=wall)

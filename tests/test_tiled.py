@@ -1,0 +1,148 @@
+"""Oversized-tile strip decomposition (BASELINE configs[4]): host logic with
+world_size 2/4 gloo groups on CPU, and device parity against the single-tile
+optimize on the GPU (ranks sharing one GPU over gloo)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2303_12529_b200 import tiled
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run(world, fn, *args, timeout=300):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=fn, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=timeout) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(out, key=lambda t: t[0])
+
+
+def test_strip_geometry():
+    for W, world, K in [(1024, 4, 35), (8192, 8, 35), (2048, 2, 17), (512, 1, 35)]:
+        strips = [tiled.strip_geometry(256, W, world, r, K) for r in range(world)]
+        covered = np.concatenate([np.arange(s.x0, s.x1) for s in strips])
+        assert np.array_equal(np.sort(covered), np.arange(W))
+        for s in strips:
+            i0, i1 = s.interior
+            assert s.ww & (s.ww - 1) == 0 and s.ww <= W
+            assert i0 >= min(s.halo, i0) and (world == 1 or (i0 >= s.halo and s.ww - i1 >= s.halo))
+            assert np.array_equal(s.columns()[i0:i1], np.arange(s.x0, s.x1))
+    s = tiled.strip_geometry(8192, 8192, 8, 3, 35)
+    assert (s.ww, s.hl, s.interior) == (2048, 512, (512, 1536))
+    assert tiled.strip_geometry(64, 1024, 4, 0, 35).stencil_bounds() == (128, 512)
+    assert tiled.strip_geometry(64, 1024, 4, 3, 35).stencil_bounds() == (0, 384)
+    with pytest.raises(ValueError):
+        tiled.strip_geometry(64, 100, 3, 0, 35)
+    with pytest.raises(ValueError):
+        tiled.strip_geometry(64, 128, 2, 0, 35)
+
+
+def _halo_worker(rank, world, port, q, W, K):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = tiled.strip_geometry(8, W, world, rank, K)
+        phi = torch.full((8, s.ww), -1.0, dtype=torch.float64)
+        i0, i1 = s.interior
+        phi[:, i0:i1] = torch.as_tensor(s.columns()[i0:i1], dtype=torch.float64)
+        tiled.exchange_halos(phi, s)
+        q.put((rank, phi.numpy(), s.columns(), s.interior, s.halo))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_halo_exchange_gloo(world):
+    W, K = 1024, 35
+    for rank, phi, cols, (i0, i1), h in _run(world, _halo_worker, W, K):
+        # interior and HALO columns on each side hold the global column index (wrapping)
+        assert np.array_equal(phi[:, i0 - h:i1 + h], np.broadcast_to(cols[i0 - h:i1 + h], (8, i1 - i0 + 2 * h)))
+
+
+# ---------------------------------------------------------------------------
+# device parity (GPU box)
+
+def _case():
+    from conftest import golden
+    kg = golden("kernels")
+    t = np.zeros((256, 1024), dtype=np.uint8)
+    t[60:200, 200:300] = 1    # crosses the 256-column strip boundaries
+    t[100:140, 480:560] = 1
+    t[30:90, 700:1000] = 1
+    return t, (kg["35_8_4_f_c"], kg["35_8_4_f_w"]), (kg["35_8_4_d_c"], kg["35_8_4_d_w"])
+
+
+def _ks(arrs, cond):
+    import paper_2303_12529_b200 as b2
+    return b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(*arrs)], cond)
+
+
+def _tiled_worker(rank, world, port, q, max_iters):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    import paper_2303_12529_b200 as b2
+    from paper_2303_12529_b200 import _native as nv
+    torch.cuda.set_device(0)
+    nv.set_precision("fp64")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t, f, d = _case()
+        r = tiled.optimize_tiled(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=max_iters))
+        h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
+        q.put((rank, h, r.final_mask, r.metrics.l2, r.metrics.pvband))
+    finally:
+        dist.destroy_process_group()
+
+
+def _reference(max_iters):
+    import paper_2303_12529_b200 as b2
+    from paper_2303_12529_b200 import _native as nv
+    nv.set_precision("fp64")
+    t, f, d = _case()
+    r = b2.optimize(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=max_iters))
+    h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
+    return h, r.final_mask, r.metrics.l2, r.metrics.pvband
+
+
+@pytest.mark.gpu
+def test_single_strip_is_bit_identical_to_optimize():
+    import paper_2303_12529_b200 as b2
+    from paper_2303_12529_b200 import _native as nv
+    nv.set_precision("fp64")
+    t, f, d = _case()
+    r = tiled.optimize_tiled(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=12))
+    h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
+    hr, mr, l2, pvb = _reference(12)
+    assert np.array_equal(h, hr)
+    assert np.array_equal(r.final_mask, mr) and (r.metrics.l2, r.metrics.pvband) == (l2, pvb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_strips_match_single_tile(world):
+    """Ranks share cuda:0 over gloo; interior results equal the full-tile run
+    up to summation order of the global reductions."""
+    hr, mr, l2, pvb = _reference(12)
+    for rank, h, mask, l2r, pvbr in _run(world, _tiled_worker, 12, timeout=600):
+        assert h.shape == hr.shape
+        assert np.allclose(h, hr, rtol=1e-9, atol=1e-12)
+        assert np.array_equal(mask, mr)
+        assert (l2r, pvbr) == (l2, pvb)
