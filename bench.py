@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-solve", action="store_true")
     p.add_argument("--clips", type=int, default=64, help="config 3 batch size (0 = skip)")
+    p.add_argument("--tile", type=int, default=8192, help="config 5 tile side, split over the ranks (0 = skip)")
+    p.add_argument("--tile-iters", type=int, default=6)
     return p.parse_args()
 
 
@@ -311,6 +313,26 @@ def b200_arm(args, world, rank, local):
                      "note": f"iccad_like_clip(0..{args.clips - 1}) round-robin over {world} GPU(s), "
                              "default OptConfig, each clip solved to the stop rule"}
 
+    # ---- config 5: one oversized tile split into strips over the ranks -------
+    tile = None
+    if args.tile > 0 and not args.no_solve:
+        from paper_2303_12529_b200 import tiled
+        T = args.tile
+        g = T // N_SIDE
+        mosaic = inputs.mosaic_tile(range(g * g), grid=(g, g)) if g >= 1 and T % N_SIDE == 0 else \
+            inputs.iccad_like_clip(seed=0, n=T)
+        cfg_t = b2.OptConfig(max_iters=args.tile_iters, stop_patience=10**9, precision=args.precision)
+        tiled.optimize_tiled(mosaic, focus, defocus, b2.OptConfig(max_iters=1, stop_patience=10**9,
+                                                                  precision=args.precision))  # warm-up
+        rt = tiled.optimize_tiled(mosaic, focus, defocus, cfg_t)
+        loop = parallel.max_over_ranks(rt.loop_time, device="cuda")
+        st = tiled.strip_geometry(T, T, world, rank, K_SIDE)
+        tile = {"side": T, "ranks": world, "window": [T, st.ww], "iters": rt.iters_run,
+                "loop_s": round(loop, 4), "iters_per_s": round(rt.iters_run / loop, 3),
+                "ms_per_iter": round(1e3 * loop / rt.iters_run, 2),
+                "note": f"{T}^2 mosaic of iccad_like_clips, full-height strips over {world} rank(s), "
+                        "34-column phi halo exchange + 4 scalar all-reduces per iteration (configs[4])"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -355,6 +377,7 @@ def b200_arm(args, world, rank, local):
         "clocks": clk.summary(),
         "solve": solve,
         "batch": batch,
+        "tile": tile,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

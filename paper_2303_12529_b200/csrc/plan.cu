@@ -171,6 +171,8 @@ int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
       throw Error(LSOPC_EINVAL, "grid " + std::to_string(W) + "x" + std::to_string(H) +
                                     " unsupported: sides must be powers of two in [4, 8192]");
     if (precision != LSOPC_FP32 && precision != LSOPC_FP64) throw Error(LSOPC_EINVAL, "bad precision");
+    if (precision == LSOPC_FP64 && (H > 4096 || W > 4096))
+      throw Error(LSOPC_EINVAL, "the FP64 tier supports sides up to 4096; use the FP32 tier for larger grids");
     auto* p = new lsopc_plan();
     try {
       p->g.H = H;

@@ -25,13 +25,14 @@ extern template int finish_impl<double>(const Grid& g, const void* V0, const voi
 using namespace spec;
 
 namespace {
-__global__ void k_embed(int K, int H, int W, const double2* __restrict__ coeffs, double2* out) {
+template <typename RC>
+__global__ void k_embed(int K, int H, int W, const double2* __restrict__ coeffs, typename CT<RC>::C* out) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= K * K) return;
   int i = t / K, j = t % K;
   int y = ((i - K / 2) % H + H) % H;
   int x = ((j - K / 2) % W + W) % W;
-  out[(size_t)y * W + x] = coeffs[t];
+  out[(size_t)y * W + x] = cmk((RC)coeffs[t].x, (RC)coeffs[t].y);
 }
 }  // namespace
 
@@ -79,57 +80,69 @@ int launch_adjoint_finish(const Grid& g, const void* V0, const void* V1, double 
   return finish_impl<float>(g, V0, V1, scale, out, vp, dots, stop, s, ix0, ix1);
 }
 
-// K0: spectra in float64 (row pass then column pass), stored column-tiled in
-// the plan's precision.  scratch, scratch2: >= H*W*16 bytes each.
-void launch_kernel_spectra(const Grid& g, int nk, int K, const double* coeffs_dev, void* spec, void* scratch,
-                           void* scratch2, cudaStream_t s) {
-  Grid g64 = g;
-  g64.prec = F64;
-  g64.tw = g.tw64;
-  Shape<double> sh = shape_of<double>(g64);
+// K0: spectra, row pass then column pass, stored column-tiled in the plan's
+// precision.  The transforms run in float64 (then round to complex64 for the
+// FP32 tier) up to 4096-point sides; an FP32 plan with a larger side (the
+// 8192^2 tile of configs[4]) transforms in float32, since one CTA holds at
+// most a 4096-point complex128 sequence (relative error ~1e-7, far inside the
+// FP32 tier's 1e-4).  scratch, scratch2: >= H*W*16 bytes each.
+template <typename RC>
+void spectra_impl(const Grid& g, int nk, int K, const double* coeffs_dev, void* spec, void* scratch, void* scratch2,
+                  cudaStream_t s) {
+  using CC = typename CT<RC>::C;
+  Grid gc = g;
+  gc.prec = sizeof(RC) == 8 ? F64 : F32;
+  gc.tw = sizeof(RC) == 8 ? g.tw64 : g.tw;
+  Shape<RC> sh = shape_of<RC>(gc);
   const size_t n = g.n();
-  const int lgT_out = g.prec == F64 ? sh.lgT : shape_of<float>(g).lgT;
+  const int lgT_out = g.prec == F64 ? shape_of<double>(g).lgT : shape_of<float>(g).lgT;
   for (int k = 0; k < nk; ++k) {
-    cudaMemsetAsync(scratch, 0, n * sizeof(double2), s);
+    cudaMemsetAsync(scratch, 0, n * sizeof(CC), s);
     const int nt = K * K;
-    k_embed<<<(nt + 255) / 256, 256, 0, s>>>(K, g.H, g.W, reinterpret_cast<const double2*>(coeffs_dev) + (size_t)k * nt,
-                                            static_cast<double2*>(scratch));
-    RowsOp<double, false> rr;
+    k_embed<RC><<<(nt + 255) / 256, 256, 0, s>>>(K, g.H, g.W, reinterpret_cast<const double2*>(coeffs_dev) + (size_t)k * nt,
+                                                static_cast<CC*>(scratch));
+    RowsOp<RC, false> rr;
     rr.sh = sh;
-    rr.in = static_cast<const double2*>(scratch);
+    rr.in = static_cast<const CC*>(scratch);
     rr.Lin = sh.rm();
     rr.Lout = sh.ct();
-    rr.out = static_cast<double2*>(scratch2);
-    rr.tw = static_cast<const double2*>(g.tw64);
+    rr.out = static_cast<CC*>(scratch2);
+    rr.tw = static_cast<const CC*>(gc.tw);
     rr.bufE = row_bufE(sh);
     rr.nitems = g.H >> sh.lgR;
-    launch_op<double>(rr, row_threads(sh), 0, nullptr, s);
+    launch_op<RC>(rr, row_threads(sh), 0, nullptr, s);
     if (g.prec == F64) {
-      ColsOp<double, double, false> cc;
+      ColsOp<RC, double, false> cc;
       cc.sh = sh;
-      cc.in = static_cast<const double2*>(scratch2);
+      cc.in = static_cast<const CC*>(scratch2);
       cc.Lin = sh.ct();
       cc.Lout = Lay{g.H, lgT_out};
       cc.out = static_cast<double2*>(spec) + (size_t)k * n;
-      cc.scale = 1.0;
-      cc.tw = static_cast<const double2*>(g.tw64);
+      cc.scale = (RC)1;
+      cc.tw = static_cast<const CC*>(gc.tw);
       cc.bufE = col_bufE(sh);
       cc.nitems = g.W >> sh.lgS;
-      launch_op<double>(cc, col_threads(sh), 0, nullptr, s);
+      launch_op<RC>(cc, col_threads(sh), 0, nullptr, s);
     } else {
-      ColsOp<double, float, false> cc;
+      ColsOp<RC, float, false> cc;
       cc.sh = sh;
-      cc.in = static_cast<const double2*>(scratch2);
+      cc.in = static_cast<const CC*>(scratch2);
       cc.Lin = sh.ct();
       cc.Lout = Lay{g.H, lgT_out};
       cc.out = static_cast<float2*>(spec) + (size_t)k * n;
-      cc.scale = 1.0;
-      cc.tw = static_cast<const double2*>(g.tw64);
+      cc.scale = (RC)1;
+      cc.tw = static_cast<const CC*>(gc.tw);
       cc.bufE = col_bufE(sh);
       cc.nitems = g.W >> sh.lgS;
-      launch_op<double>(cc, col_threads(sh), 0, nullptr, s);
+      launch_op<RC>(cc, col_threads(sh), 0, nullptr, s);
     }
   }
+}
+
+void launch_kernel_spectra(const Grid& g, int nk, int K, const double* coeffs_dev, void* spec, void* scratch,
+                           void* scratch2, cudaStream_t s) {
+  if (g.prec == F32 && std::max(g.H, g.W) > 4096) spectra_impl<float>(g, nk, K, coeffs_dev, spec, scratch, scratch2, s);
+  else spectra_impl<double>(g, nk, K, coeffs_dev, spec, scratch, scratch2, s);
 }
 
 // spectrum field (plan precision, column-tiled) -> complex128 row-major

@@ -1052,14 +1052,21 @@ template <typename R> int row_threads(const Shape<R>& sh) {
   using C = typename CT<R>::C;
   return std::max(1, ((1 << sh.lgR) << sh.lgW) / eng::P_of<C>());
 }
+// stage-buffer sizes are rounded to 128 B so every ring slot stays aligned for
+// 16 B cp.async and TMA destinations
+template <typename R> int align_elems(int e) {
+  using C = typename CT<R>::C;
+  const int q = 128 / (int)sizeof(C);
+  return (e + q - 1) / q * q;
+}
 template <typename R> int col_bufE(const Shape<R>& sh) {
   using C = typename CT<R>::C;
-  return eng::buf_elems<C>(sh.H, 1 << sh.lgS);
+  return align_elems<R>(eng::buf_elems<C>(sh.H, 1 << sh.lgS));
 }
 template <typename R> int row_bufE(const Shape<R>& sh) {
   using C = typename CT<R>::C;
   // the mask pass stages raw f64 input (8 B/elem) in a complex buffer
-  return std::max(eng::buf_elems<C>(sh.W, 1 << sh.lgR), (int)(((1 << sh.lgR) << sh.lgW) * 8 / sizeof(C)));
+  return align_elems<R>(std::max(eng::buf_elems<C>(sh.W, 1 << sh.lgR), (int)(((1 << sh.lgR) << sh.lgW) * 8 / sizeof(C))));
 }
 
 template <typename R> SetArgs<R> set_args(const Grid& g, const SpecSet* sets, int nsets) {

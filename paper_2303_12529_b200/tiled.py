@@ -156,6 +156,7 @@ class TiledResult:
     loss_history: list
     iters_run: int
     wall_time: float
+    loop_time: float = 0.0      # seconds in the iteration loop (device-synchronised)
 
 
 def optimize_tiled(target, focus_kernels, defocus_kernels, cfg, phi0=None):
@@ -207,6 +208,8 @@ def optimize_tiled(target, focus_kernels, defocus_kernels, cfg, phi0=None):
         phi = torch.as_tensor(_CudaView(L.lsopc_session_phi_ptr(sess), (H, st.ww), "<f8"), device="cuda")
         flag = torch.as_tensor(_CudaView(L.lsopc_session_state_flag(sess), (1,), "<i4"), device="cuda")
         SUM, MAX = dist.ReduceOp.SUM, dist.ReduceOp.MAX
+        torch.cuda.synchronize()
+        t_loop = time.perf_counter()
         for _ in range(cfg.max_iters):
             nv.check(L.lsopc_session_phase(sess, 0))
             all_reduce_(sc[0:2], SUM)
@@ -220,6 +223,8 @@ def optimize_tiled(target, focus_kernels, defocus_kernels, cfg, phi0=None):
             if int(flag.item()):   # identical on every rank (same global scalars)
                 break
             exchange_halos(phi, st)
+        torch.cuda.synchronize()
+        t_loop = time.perf_counter() - t_loop
         best = nv.empty((H, st.ww), np.float64)
         fmask = nv.empty((H, st.ww), np.uint8)
         hist = np.zeros((cfg.max_iters + 1, 7))
@@ -256,4 +261,5 @@ def optimize_tiled(target, focus_kernels, defocus_kernels, cfg, phi0=None):
     report = MetricsReport(l2=int(counts[0].item()), pvband=int(counts[1].item()), shots=shot_count(final_mask),
                            wall_time=wall, iters=res.iters)
     return TiledResult(final_mask=final_mask, final_phi=LevelSetField(final_phi, cfg.d_upper, cfg.d_lower),
-                       metrics=report, loss_history=history, iters_run=res.iters, wall_time=wall)
+                       metrics=report, loss_history=history, iters_run=res.iters, wall_time=wall,
+                       loop_time=t_loop)
