@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--clips", type=int, default=64, help="config 3 batch size (0 = skip)")
     p.add_argument("--tile", type=int, default=8192, help="config 5 tile side, split over the ranks (0 = skip)")
     p.add_argument("--tile-iters", type=int, default=6)
+    p.add_argument("--dsn-batch", type=int, default=16, help="config 4 batch (0 = skip)")
     return p.parse_args()
 
 
@@ -313,6 +314,24 @@ def b200_arm(args, world, rank, local):
                      "note": f"iccad_like_clip(0..{args.clips - 1}) round-robin over {world} GPU(s), "
                              "default OptConfig, each clip solved to the stop rule"}
 
+    # ---- config 4: DevelSet-Net (random init) + GPU level-set refinement -----
+    instant = None
+    if args.dsn_batch > 0 and not args.no_solve:
+        from paper_2303_12529_b200 import dsn
+        net = dsn.build_net()
+        cfg_d = b2.OptConfig(precision=args.precision)
+        dsn.instant_opc([inputs.iccad_like_clip(seed=900)], focus, defocus, cfg_d, net=net)  # warm-up
+        batch_t = [inputs.iccad_like_clip(seed=500 + rank * args.dsn_batch + i) for i in range(args.dsn_batch)]
+        ri = dsn.instant_opc(batch_t, focus, defocus, cfg_d, net=net)
+        lat = parallel.max_over_ranks(ri.latency, device="cuda")
+        instant = {"batch": args.dsn_batch, "latency_s": round(lat, 4),
+                   "stages_s": {"tsdf": round(ri.t_tsdf, 4), "dsn": round(ri.t_net, 4),
+                                "init": round(ri.t_init, 4), "dso": round(ri.t_dso, 4)},
+                   "iters_total": int(sum(x.iters_run for x in ri.results)),
+                   "mean_l2": round(float(np.mean([x.metrics.l2 for x in ri.results])), 1),
+                   "note": "random-init two-branch UNet (bf16) -> fused clip + AHF -> DSO per clip to the stop "
+                           "rule (configs[3]); per rank"}
+
     # ---- config 5: one oversized tile split into strips over the ranks -------
     tile = None
     if args.tile > 0 and not args.no_solve:
@@ -378,6 +397,7 @@ def b200_arm(args, world, rank, local):
         "solve": solve,
         "batch": batch,
         "tile": tile,
+        "instant_opc": instant,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

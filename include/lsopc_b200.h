@@ -176,6 +176,13 @@ int lsopc_session_phi(lsopc_session* s, double* phi_dev);
 /* Number of kernel launches one DSO iteration enqueues (bench accounting). */
 int lsopc_session_launches_per_iter(const lsopc_session* s);
 
+/* DevelSet-Net front end -> DSO initial state in one pass (configs[3];
+ * PAPER.md:553-635, boundary optimizer.py:215-228): phi0 = clip(phi_raw,
+ * d_lower, d_upper) and m = AHF_epsilon(m_raw) = (1 + (2/pi) atan(m_raw/eps))/2
+ * (levelset.py:147-151); float32 network outputs, float64 results. */
+int lsopc_dsn_init(size_t n, const float* phi_raw_dev, const float* m_raw_dev, double d_lower, double d_upper,
+                   double epsilon, double* phi0_dev, double* m_dev, void* stream);
+
 /* Oversized tile split across ranks into full-height strips (BASELINE
  * configs[4]).  The session's grid is this rank's window: its
  * interior columns [ix0, ix1) plus halo columns refreshed from the

@@ -45,6 +45,8 @@ void launch_ls_velocity(int H, int W, const double* phi, const double* v, const 
                         double* partials, Tile t, cudaStream_t s);
 void launch_ls_update(int H, int W, double* phi, const double* u, const double* gm, double lo, double hi,
                       const DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s);
+void launch_dsn_init(size_t n, const float* phi_raw, const float* m_raw, double lo, double hi, double eps,
+                     double* phi0, double* m, cudaStream_t s);
 // fixed-order reduction of nb blocks of nv partials (sum or max) into out[0..nv)
 void launch_reduce_partials(const double* part, int nb, int nv, int is_max, double* out, cudaStream_t s);
 void launch_copy_best(size_t n, const double* phi, double* best, const DevState* st, cudaStream_t s);

@@ -322,6 +322,17 @@ __global__ void k_elementwise(int op, size_t n, const double* __restrict__ a, co
   }
 }
 
+// DevelSet-Net outputs -> DSO inputs in one pass (boundary
+// optimizer.py:215-228): phi0 = clip(phi_raw, D_l, D_u), m = AHF_eps(m_raw)
+// (levelset.py:147-151), float32 network outputs widened to float64.
+__global__ void k_dsn_init(size_t n, const float* __restrict__ phi_raw, const float* __restrict__ m_raw,
+                           double lo, double hi, double eps, double* phi0, double* m) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    phi0[i] = fmin(fmax((double)phi_raw[i], lo), hi);
+    m[i] = mul(0.5, add(1.0, mul(2.0 / CUDART_PI, atan(dvd((double)m_raw[i], eps)))));
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
 k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restrict__ b,
          const uint8_t* __restrict__ a8, const uint8_t* __restrict__ b8, double* partials, int W, int ix0, int ix1) {
@@ -399,6 +410,10 @@ void launch_after_velocity(const double* part, int nb, double eta, DevState* st,
 }
 void launch_after_update(const double* part, int nb, DevState* st, double* hist, cudaStream_t s) {
   k_after_update<<<1, 256, 0, s>>>(part, nb, st, hist);
+}
+void launch_dsn_init(size_t n, const float* phi_raw, const float* m_raw, double lo, double hi, double eps,
+                     double* phi0, double* m, cudaStream_t s) {
+  k_dsn_init<<<kBlocks, kThreads, 0, s>>>(n, phi_raw, m_raw, lo, hi, eps, phi0, m);
 }
 void launch_reduce_partials(const double* part, int nb, int nv, int is_max, double* out, cudaStream_t s) {
   if (nv == 1) {

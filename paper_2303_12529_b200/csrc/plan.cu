@@ -792,6 +792,18 @@ int lsopc_session_destroy(lsopc_session* ss) {
   });
 }
 
+int lsopc_dsn_init(size_t n, const float* phi_raw_dev, const float* m_raw_dev, double d_lower, double d_upper,
+                   double epsilon, double* phi0_dev, double* m_dev, void* stream) {
+  return guarded([&] {
+    if (!(d_lower < 0.0 && 0.0 < d_upper)) throw Error(LSOPC_EINVAL, "truncation bounds must satisfy D_l < 0 < D_u");
+    if (!(epsilon > 0.0)) throw Error(LSOPC_EINVAL, "epsilon must be positive");
+    if (n == 0) return;
+    launch_dsn_init(n, phi_raw_dev, m_raw_dev, d_lower, d_upper, epsilon, phi0_dev, m_dev,
+                    static_cast<cudaStream_t>(stream));
+    ck_launch("dsn init");
+  });
+}
+
 int lsopc_session_set_tile(lsopc_session* ss, int ix0, int ix1, int xlo, int xhi) {
   return guarded([&] {
     if (!ss) throw Error(LSOPC_EINVAL, "null session");

@@ -262,17 +262,39 @@ def _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation):
     return target, m, fk, dk
 
 
+def _is_device_tensor(x):
+    return x is not None and hasattr(x, "is_cuda") and x.is_cuda
+
+
+def _device_f64(x, shape):
+    if x is None:
+        return None
+    if tuple(x.shape) != tuple(shape):
+        raise ValueError("device initial state does not match the target shape")
+    return x.to(dtype=nv.torch().float64).contiguous()
+
+
 def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=None):
     """Device part of `optimize`: the loop, final prints and the device-to-host
     copies.  Returns the pieces `_assemble` turns into an OptimizationResult
     (split so a batch driver can overlap one clip's host tail with the next
     clip's device loop)."""
     t0 = time.perf_counter()
-    target, m, fk, dk = _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
+    if _is_device_tensor(phi0) or _is_device_tensor(modulation):
+        # device-resident initial state (DevelSet-Net front end, dsn.py): the
+        # caller has already clipped phi0 and mapped m through the AHF on the device
+        target = _check_target(target)
+        fk = litho.device_kernels(focus_kernels, target.shape, cfg.precision)
+        dk = litho.device_kernels(defocus_kernels, target.shape, cfg.precision)
+        m = None
+        p0 = _device_f64(phi0, target.shape)
+        mdv = _device_f64(modulation, target.shape)
+    else:
+        target, m, fk, dk = _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
+        p0 = nv.to_dev(phi0.phi) if phi0 is not None else None
+        mdv = nv.to_dev(m) if m is not None else None
     shape = target.shape
     td = nv.to_dev(target, np.uint8)
-    p0 = nv.to_dev(phi0.phi) if phi0 is not None else None
-    mdv = nv.to_dev(m) if m is not None else None
     best = nv.empty(shape, np.float64)
     fmask = nv.empty(shape, np.uint8)
     hist = np.zeros((cfg.max_iters + 1, 7))
@@ -299,7 +321,7 @@ def _assemble(parts, cfg, phi0=None):
     shots = shot_count(final_mask)
     history = [IterationRecord(*(float(v) for v in row)) for row in hist[:iters]]
     bounds = (cfg.d_upper, cfg.d_lower)
-    if phi0 is not None:
+    if phi0 is not None and not _is_device_tensor(phi0):
         # the initial iterate keeps phi0's own bounds (optimizer.py:219-220,231);
         # the best iterate is the first strict minimum of the recorded losses
         losses = [h.l_dso for h in history]
