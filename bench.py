@@ -195,9 +195,16 @@ def b200_arm(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # BENCH_DIST_BACKEND=gloo + BENCH_DEVICE=0 run several ranks on one GPU
+    # (a functional check of the multi-rank paths; timings are then shared-GPU)
+    dev = int(os.environ.get("BENCH_DEVICE", local))
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     import paper_2303_12529_b200 as b2
     from paper_2303_12529_b200 import _native as nv
     from paper_2303_12529_b200 import inputs, parallel
@@ -231,7 +238,7 @@ def b200_arm(args, world, rank, local):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         ev0.record(stream)
         nv.check(L.lsopc_session_enqueue(sess, K))
         ev1.record(stream)

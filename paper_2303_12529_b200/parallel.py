@@ -50,6 +50,8 @@ def max_over_ranks(value, group=None, device=None):
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return float(value)
+    if dist.get_backend(group) != "nccl":
+        device = "cpu"  # gloo reduces host tensors
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
