@@ -25,6 +25,9 @@
 // conflicts.  Radix-16 stages for complex64 (16 values per thread), radix-8
 // for complex128 (8 values per thread).
 #pragma once
+#include <type_traits>
+#include <utility>
+
 #include "common.cuh"
 
 namespace eng {
@@ -316,6 +319,11 @@ LS_D int xaddr_t(int seq, int base, int r) {
   else return seq * LD + pidx;
 }
 
+// optional functor hook run by every thread just before the last stage's
+// stores (e.g. waiting for an operand the stores consume)
+template <class F, class = void> struct has_pre_store : std::false_type {};
+template <class F> struct has_pre_store<F, std::void_t<decltype(std::declval<F&>().pre_store())>> : std::true_type {};
+
 template <int LGN, int LGS, int LGR, int LGNS, bool FIRST, bool LAST, bool COLS, bool INV, typename C, class F>
 LS_D void stage_t(C (&v)[P_of<C>()], C* sm, const C* __restrict__ tw, int tws, F& f) {
   constexpr int RAD = 1 << LGR, P = P_of<C>();
@@ -346,6 +354,7 @@ LS_D void stage_t(C (&v)[P_of<C>()], C* sm, const C* __restrict__ tw, int tws, F
     dft<RAD>(&v[i * RAD]);
   }
   __syncthreads();
+  if constexpr (LAST && has_pre_store<F>::value) f.pre_store();
 #pragma unroll
   for (int i = 0; i < P / RAD; ++i) {
     const int b = threadIdx.x + i * NT;

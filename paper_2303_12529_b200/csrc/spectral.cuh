@@ -718,12 +718,12 @@ __global__ void __launch_bounds__(512, 1) k_pass_tma(const __grid_constant__ Op 
 #endif
   extern __shared__ __align__(128) unsigned char smraw[];
   C* const base = reinterpret_cast<C*>(smraw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 3 * (size_t)op.bufE * sizeof(C));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 3 * (size_t)op.bufE * sizeof(C));  // 3 ring + 1 side
   typename Op::State S{};
   if ((int)blockIdx.x >= op.nitems) return;
   const bool leader = threadIdx.x == 0;
   if (leader) {
-    for (int i = 0; i < 3; ++i) tma::mbar_init(&bar[i], 1);
+    for (int i = 0; i < 4; ++i) tma::mbar_init(&bar[i], 1);
     tma::fence_mbar_init();
   }
   __syncthreads();
@@ -739,15 +739,22 @@ __global__ void __launch_bounds__(512, 1) k_pass_tma(const __grid_constant__ Op 
   advance(nit, nst);
   for (unsigned q = 0;; ++q) {
     const int slot = q % 3, nslot = (q + 1) % 3;
+    C* const side = base + ((q + 2) % 3) * op.bufE;  // idle slot when the op stores nothing
     if (leader && nit < op.nitems) {
       if (Op::kStores) tma::bulk_wait_read<1>();  // slot nslot held the stores of step q-2
       tma::mbar_expect_tx(&bar[nslot], op.load_bytes());
       op.load(nit, nst, base + nslot * op.bufE, &bar[nslot]);
     }
+    if constexpr (Op::kSideLoad) {
+      if (leader) {
+        tma::mbar_expect_tx(&bar[3], op.load_bytes());
+        op.side_load(it, st, side, &bar[3]);
+      }
+    }
     tma::mbar_wait(&bar[slot], (q / 3) & 1);
     C* const cur = base + slot * op.bufE;
     if (st == 0) op.begin(S, it, cur);
-    op.step(S, it, st, cur, cur);
+    op.step(S, it, st, cur, side, q);
     if (Op::kStores) {
       tma::fence_async_smem();
       __syncthreads();
@@ -778,6 +785,7 @@ template <typename R> struct TF1Op : OpBase {
   using C = typename CT<R>::C;
   static constexpr int P = eng::P_of<C>();
   static constexpr bool kStores = true;
+  static constexpr bool kSideLoad = false;
   using State = typename F1Op<R>::State;
   Shape<R> sh;
   SetArgs<R> a;
@@ -828,7 +836,7 @@ template <typename R> struct TF1Op : OpBase {
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, true>(seq, j, r)] = v; }
   };
-  LS_D void step(State& S, int, int, C* b, C*) const {
+  LS_D void step(State& S, int, int, C* b, C*, unsigned) const {
     const Geo g = sh.gcol();
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -845,6 +853,7 @@ template <typename R> struct TF2Op : OpBase {
   using C = typename CT<R>::C;
   static constexpr int P = eng::P_of<C>();
   static constexpr bool kStores = true;
+  static constexpr bool kSideLoad = false;
   using State = typename F2Op<R>::State;
   Shape<R> sh;
   SetArgs<R> a;
@@ -880,7 +889,7 @@ template <typename R> struct TF2Op : OpBase {
       b[nat_out<LGN, ST, C, false>(seq, j, r)] = v;
     }
   };
-  LS_D void step(State& S, int it, int k, C* b, C*) const {
+  LS_D void step(State& S, int it, int k, C* b, C*, unsigned) const {
     const Geo g = sh.grow();
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -905,6 +914,7 @@ template <typename R> struct TA1Op : OpBase {
   using C = typename CT<R>::C;
   static constexpr int P = eng::P_of<C>();
   static constexpr bool kStores = true;
+  static constexpr bool kSideLoad = false;
   using State = typename A1Op<R>::State;
   Shape<R> sh;
   SetArgs<R> a;
@@ -943,7 +953,7 @@ template <typename R> struct TA1Op : OpBase {
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, false>(seq, j, r)] = v; }
   };
-  LS_D void step(State& S, int, int, C* b, C*) const {
+  LS_D void step(State& S, int, int, C* b, C*, unsigned) const {
     const Geo g = sh.grow();
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -955,22 +965,67 @@ template <typename R> struct TA1Op : OpBase {
   }
 };
 
-// TA2: V_set = IFFT_y(sum_k w_k conj(H_k) FFT_y U_k): U_k tile in by TMA
+// TA2: V_set = IFFT_y(sum_k w_k conj(H_k) FFT_y U_k).  U_k tiles arrive in the
+// ring; since the pass stores nothing per step, the ring's third slot is idle
+// and takes H_k of the current step (TMA, own mbarrier), which the last
+// butterfly stage reads from shared memory.
 template <typename R> struct TA2Op : A2Op<R> {
   using C = typename CT<R>::C;
+  using State = typename A2Op<R>::State;
+  static constexpr int P = eng::P_of<C>();
   static constexpr bool kStores = false;
+  static constexpr bool kSideLoad = true;
   int u_lgw;
-  alignas(64) CUtensorMap tmap_U;  // U fields, column-item boxes
+  alignas(64) CUtensorMap tmap_U;     // U fields, column-item boxes
+  alignas(64) CUtensorMap tmap_spec;  // spectra of set 0, column-item boxes
+  alignas(64) CUtensorMap tmap_spec1; // spectra of set 1
   int koff[2];
   LS_D unsigned load_bytes() const { return (unsigned)((this->sh.H << this->sh.lgS) * sizeof(C)); }
-  LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
-    const int set = it >> this->lgnt, x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
+  template <class Fn> LS_D void col_boxes(int x0, Fn&& fn) const {
     const int ew = sizeof(C) / 8, w = 1 << u_lgw, S = 1 << this->sh.lgS;
     const int rows = this->sh.H < 256 ? this->sh.H : 256;
-    for (int b = 0; b * rows < this->sh.H; ++b)
-      tma::tensor_g2s(dst + b * rows * S, &tmap_U, (x0 & (w - 1)) * ew, x0 >> u_lgw, b * rows, k + koff[set], bar);
+    for (int b = 0; b * rows < this->sh.H; ++b) fn((x0 & (w - 1)) * ew, x0 >> u_lgw, b * rows, b * rows * S);
+  }
+  LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
+    const int set = it >> this->lgnt, x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
+    col_boxes(x0, [&](int c0, int c1, int c2, int off) {
+      tma::tensor_g2s(dst + off, &tmap_U, c0, c1, c2, k + koff[set], bar);
+    });
+  }
+  LS_D void side_load(int it, int k, C* dst, uint64_t* bar) const {
+    const int set = it >> this->lgnt, x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
+    const CUtensorMap* m = set ? &tmap_spec1 : &tmap_spec;
+    col_boxes(x0, [&](int c0, int c1, int c2, int off) { tma::tensor_g2s(dst + off, m, c0, c1, c2, k, bar); });
   }
   LS_D void store(int, int, const C*) const {}
+  // the side-load mbarrier: 4th barrier behind the ring (k_pass_tma's layout)
+  LS_D uint64_t* side_bar() const {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    return reinterpret_cast<uint64_t*>(smraw + 3 * (size_t)this->bufE * sizeof(C)) + 3;
+  }
+  template <int LGN> struct F {
+    const C* b;
+    const C* h;     // H_k tile (natural [y][S]) in the side slot
+    uint64_t* bar;  // its mbarrier
+    unsigned parity;
+    State& S;
+    R w;
+    LS_D void pre_store() const { tma::mbar_wait(bar, parity); }
+    template <int ST> LS_D C load(int seq, int j, int r, int) const { return b[nat_col<LGN, ST, C>(seq, j, r, 0)]; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int slot) {
+      S.acc[slot] = S.acc[slot] + cmulc(v, h[nat_col<LGN, ST, C>(seq, j, r, 0)]) * w;
+    }
+  };
+  LS_D void step(State& S, int it, int k, C* b, C* side, unsigned q) const {
+    const Geo g = this->sh.gcol();
+    eng::dispatch<C>(g, true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) {
+        F<LGN> f{b, side, side_bar(), q & 1u, S, this->a.w[it >> this->lgnt][k]};
+        eng::run_fix<LGN, true, false>(g, b, this->tw, f);
+      }
+    });
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -1016,7 +1071,7 @@ int launch_op(Op& op, int threads, int extra_bufs, StopFlag stop, cudaStream_t s
 template <typename R, class Op>
 int launch_tma(Op& op, int threads, StopFlag stop, cudaStream_t s) {
   using C = typename CT<R>::C;
-  const size_t smem = 3 * (size_t)op.bufE * sizeof(C) + 3 * sizeof(uint64_t);
+  const size_t smem = 3 * (size_t)op.bufE * sizeof(C) + 4 * sizeof(uint64_t);
   if (smem > 227 * 1024) throw std::runtime_error("TMA pass needs more than 227 KB of shared memory");
   auto kern = k_pass_tma<R, Op>;
   static int per_sm = -1;
@@ -1236,6 +1291,12 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
     const int ew = sizeof(C) / 8, S = 1 << sh.lgS, w = 1 << sh.lgT;
     a2.tmap_U = make_field_map(TmaField{a.T[0], sh.lgT, ew}, g.H, g.W, total_nk(a), (unsigned)(std::min(S, w) * ew),
                                (unsigned)std::max(1, S / w), (unsigned)std::min(g.H, 256));
+    for (int i = 0; i < nsets; ++i) {
+      CUtensorMap m = make_field_map(TmaField{a.spec[i], sh.lgT, ew}, g.H, g.W, a.nk[i],
+                                     (unsigned)(std::min(S, w) * ew), (unsigned)std::max(1, S / w),
+                                     (unsigned)std::min(g.H, 256));
+      if (i == 0) a2.tmap_spec = m; else a2.tmap_spec1 = m;
+    }
     for (int i = 0; i < 2; ++i) a2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     a2.bufE = tma_bufE<R>(col_bufE(sh));
     a2.nitems = (1 << a2.lgnt) * nsets;
