@@ -172,7 +172,7 @@ _pinned = {}
 def pinned_like(t):
     """A cached page-locked host tensor with t's shape and dtype (staging for
     fast device-to-host copies; callers copy out of it before reuse)."""
-    key = (tuple(t.shape), t.dtype)
+    key = (tuple(t.shape), t.dtype, lane())
     buf = _pinned.get(key)
     if buf is None:
         buf = torch().empty(t.shape, dtype=t.dtype, pin_memory=True)
@@ -228,11 +228,23 @@ class Plan:
 
 
 _plans = {}
+_tls = threading.local()
+
+
+def set_lane(lane):
+    """Select this thread's lane: work buffers (plans) and device spectra are
+    kept per (shape, precision, lane), so threads on different lanes and
+    different CUDA streams can run solves concurrently (parallel.py)."""
+    _tls.lane = int(lane)
+
+
+def lane():
+    return getattr(_tls, "lane", 0)
 
 
 def plan_for(shape, prec):
     H, W = int(shape[0]), int(shape[1])
-    key = (H, W, prec)
+    key = (H, W, prec, lane())
     p = _plans.get(key)
     if p is None:
         for n in (H, W):

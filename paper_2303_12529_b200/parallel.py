@@ -69,16 +69,15 @@ def gather_records(records, group=None):
 
 
 def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, solver=None,
-                   synchronize=None):
+                   synchronize=None, lanes=2):
     """Solve every clip of `targets` (a sequence of 2-D uint8 layouts; a
     `LazyClips` lets each rank generate only its own clips) on the rank that
     owns it.  Returns (records of all clips ordered by index,
     seconds = max over ranks of this rank's solve time).
 
     `solver(target, focus, defocus, cfg) -> OptimizationResult` replaces the
-    device loop (tests inject a stub).  Without it, clips run through
-    `optimizer.optimize`'s two halves, with each clip's host tail (shot count,
-    records) overlapping the next clip's device loop.
+    device loop (tests inject a stub).  Without it, `lanes` concurrent
+    streams each solve every lanes-th clip of this rank's shard.
     """
     rank, world = world_info(group)
     mine = [(i, targets[i]) for i in shard(len(targets), rank, world)]  # inputs built before timing
@@ -96,22 +95,59 @@ def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, sol
         for i, target in mine:
             record(i, solver(target, focus_kernels, defocus_kernels, cfg))
     else:
-        # device loop of clip i+1 overlaps the host tail (shot count, records) of clip i
+        # `lanes` worker threads, each with its own CUDA stream and work
+        # buffers (nv.set_lane), solve alternate clips: one lane's host-side
+        # gaps (session set-up, stop-flag polls, copies, shot count) overlap
+        # the other lane's device loop.
+        import threading
         from concurrent.futures import ThreadPoolExecutor
+
+        import torch
+
+        from . import _native as nv
         from .optimizer import _assemble, _optimize_device
-        with ThreadPoolExecutor(max_workers=1) as pool:
-            pending = None
-            for i, target in mine:
-                parts = _optimize_device(target, focus_kernels, defocus_kernels, cfg)
-                if pending is not None:
-                    record(pending[0], pending[1].result())
-                pending = (i, pool.submit(_assemble, parts, cfg))
-            if pending is not None:
-                record(pending[0], pending[1].result())
+        lock = threading.Lock()
+        dev = torch.cuda.current_device()
+
+        def worker(lane, items):
+            nv.set_lane(lane)
+            torch.cuda.set_device(dev)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                for i, target in items:
+                    r = _assemble(_optimize_device(target, focus_kernels, defocus_kernels, cfg), cfg)
+                    with lock:
+                        record(i, r)
+            stream.synchronize()
+
+        with ThreadPoolExecutor(max_workers=lanes) as pool:
+            for f in [pool.submit(worker, l, mine[l::lanes]) for l in range(lanes)]:
+                f.result()
     if synchronize:
         synchronize()
     seconds = max_over_ranks(time.perf_counter() - t0, group)
     return gather_records(records, group), seconds
+
+
+def warm_lanes(target, focus_kernels, defocus_kernels, cfg, lanes=2):
+    """Solve `target` once on every lane (no collectives), so the lanes'
+    spectra, work buffers and captured iteration graphs exist before timing."""
+    import torch
+
+    from . import _native as nv
+    from .optimizer import optimize
+    dev = torch.cuda.current_device()
+    for lane in range(lanes):
+        prev = nv.lane()
+        nv.set_lane(lane)
+        try:
+            torch.cuda.set_device(dev)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                optimize(target, focus_kernels, defocus_kernels, cfg)
+            stream.synchronize()
+        finally:
+            nv.set_lane(prev)
 
 
 class LazyClips:
