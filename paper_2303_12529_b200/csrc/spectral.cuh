@@ -72,7 +72,7 @@ template <typename R> struct Shape {
 
 template <typename R> Shape<R> shape_of(const Grid& g) {
   using C = typename CT<R>::C;
-  const int E = 512 * eng::P_of<C>();
+  const int E = eng::cta_threads<C>() * eng::P_of<C>();
   Shape<R> s;
   s.H = g.H; s.W = g.W; s.lgH = g.lgH; s.lgW = g.lgW;
   s.lgS = std::max(0, std::min(g.lgW, ilog2i(E) - g.lgH));
@@ -98,7 +98,7 @@ __global__ void k_ct_to_c128(size_t n, Lay L, int W, const typename CT<R>::C* __
 // step q+1 stream in (cp.async) while step q is transformed.
 
 template <typename R, class Op>
-__global__ void __launch_bounds__(512, 1) k_pass(Op op, StopFlag stop) {
+__global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pass(Op op, StopFlag stop) {
   using C = typename CT<R>::C;
   constexpr int NB = Op::kStages;  // ring of stage buffers: prefetch distance NB - 1
 #if !defined(LSB_EXP_NOSTORE) && !defined(LSB_EXP_NOGATHER)
@@ -711,7 +711,8 @@ template <typename R> bool tma_ok(const Shape<R>& sh) {
 }
 
 template <typename R, class Op>
-__global__ void __launch_bounds__(512, 1) k_pass_tma(const __grid_constant__ Op op, StopFlag stop) {
+__global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pass_tma(const __grid_constant__ Op op,
+                                                                                       StopFlag stop) {
   using C = typename CT<R>::C;
 #if !defined(LSB_EXP_NOSTORE) && !defined(LSB_EXP_NOGATHER)
   if (stop && *stop) return;
