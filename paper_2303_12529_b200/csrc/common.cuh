@@ -33,6 +33,29 @@ template <typename C> LS_HD C cconj(C a) { return cmk(a.x, -a.y); }
 template <typename C> LS_HD C mul_mi(C a) { return cmk(a.y, -a.x); }
 
 // ---------------------------------------------------------------------------
+// flat pixel index -> (row, column) without a 64-bit divide: a shift and mask
+// for power-of-two widths (every plan grid), a 32-bit divide otherwise.
+struct RowSplit {
+  uint32_t w, mask;
+  int sh;  // log2(w), or -1 when w is not a power of two
+};
+LS_HD RowSplit row_split(int W) {
+  RowSplit r{(uint32_t)W, (uint32_t)W - 1u, -1};
+  if (W > 0 && (W & (W - 1)) == 0) {
+    int s = 0;
+    while ((1 << s) < W) ++s;
+    r.sh = s;
+  }
+  return r;
+}
+LS_D uint32_t col_of(const RowSplit& r, size_t i) {
+  return r.sh >= 0 ? (uint32_t)i & r.mask : (uint32_t)(i % r.w);
+}
+LS_D uint32_t row_of(const RowSplit& r, size_t i) {
+  return r.sh >= 0 ? (uint32_t)(i >> r.sh) : (uint32_t)(i / r.w);
+}
+
+// ---------------------------------------------------------------------------
 // deterministic reductions: warp shuffle -> smem -> one value per block; the
 // per-block partials are combined later by a single block in fixed order.
 

@@ -98,8 +98,9 @@ __global__ void __launch_bounds__(kThreads)
 k_geometry(int H, int W, const double* __restrict__ phi, double* gx, double* gy, double* gxx, double* gyy,
            double* gxy, double* mag) {
   const size_t n = (size_t)H * W;
+  const RowSplit rs = row_split(W);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    int y = (int)(i / W), x = (int)(i % W);
+    const int y = (int)row_of(rs, i), x = (int)col_of(rs, i);
     Geom g = geometry_at(phi, H, W, y, x);
     if (gx) { gx[i] = g.gx; gy[i] = g.gy; gxx[i] = g.gxx; gyy[i] = g.gyy; gxy[i] = g.gxy; }
     if (mag) mag[i] = np_hypot(g.gx, g.gy);
@@ -110,8 +111,9 @@ __global__ void __launch_bounds__(kThreads)
 k_curvature(int H, int W, const double* __restrict__ phi, const double* __restrict__ m, double weight,
             double* out) {
   const size_t n = (size_t)H * W;
+  const RowSplit rs = row_split(W);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    int y = (int)(i / W), x = (int)(i % W);
+    const int y = (int)row_of(rs, i), x = (int)col_of(rs, i);
     double k = curvature_of(geometry_at(phi, H, W, y, x), weight);
     out[i] = m ? mul(k, m[i]) : k;
   }
@@ -131,8 +133,9 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
   const double beta = st->beta;
   const size_t n = (size_t)H * W;
   double mx[2] = {0.0, 0.0};  // max |v_total|, max |grad phi|
+  const RowSplit rs = row_split(W);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    int y = (int)(i / W), x = (int)(i % W);
+    const int y = (int)row_of(rs, i), x = (int)col_of(rs, i);
     Geom g = geometry_at(phi, H, W, y, x, tl.xlo, tl.xhi);
     double gm = np_hypot(g.gx, g.gy);
     double d = -v[i];
@@ -171,8 +174,10 @@ k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const doubl
   const double dt = st->dt;
   const size_t n = (size_t)H * W;
   double mx[1] = {0.0};
+  const RowSplit rs = row_split(W);
+  const bool whole = tl.ix0 <= 0 && tl.ix1 >= W;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int x = (int)(i % W);
+    const int x = whole ? 0 : (int)col_of(rs, i);
     if (x < tl.ix0 || x >= tl.ix1) continue;  // strip halo: owned by a neighbour rank
     double step, p;
     if (gm) {  // optimizer.py:329: phi - dt * v_total * grad_mag
@@ -345,7 +350,10 @@ k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restric
       case RD_DOTDIFF: acc[0] += a[i] * (a[i] - b[i]); break;
       case RD_MAXABS: acc[0] = fmax(acc[0], fabs(a[i])); break;
       case RD_COUNTNEQ8:  // b8 null: vs 0; W > 0: columns [ix0, ix1) only
-        if (W > 0 && ((int)(i % W) < ix0 || (int)(i % W) >= ix1)) break;
+        if (W > 0) {
+          const int x = (int)col_of(row_split(W), i);
+          if (x < ix0 || x >= ix1) break;
+        }
         acc[0] += (a8[i] != (b8 ? b8[i] : 0)) ? 1.0 : 0.0;
         break;
       case RD_COUNTNEQ: acc[0] += (a[i] != b[i]) ? 1.0 : 0.0; break;

@@ -29,6 +29,8 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
   if (stop && *stop) return;
   double acc[2] = {0.0, 0.0};
   const bool have_t = tu8 || tf;
+  const RowSplit rs = row_split(W);
+  const bool whole = ix0 <= 0 && ix1 >= W;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     // litho.py:125-126: I = max(dose * sum, 0); corners: litho.py:147-149
     double sf = (double)If[i];
@@ -52,7 +54,7 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
     if (have_t) {
       double zt = tu8 ? (double)tu8[i] : tf[i];
       double dn = zn - zt, di = zi - zt, dout = zo - zt;
-      const int x = (int)(i % W);
+      const int x = whole ? ix0 : (int)col_of(rs, i);
       if (x >= ix0 && x < ix1) {         // strip interior (the whole row by default)
         acc[0] += dn * dn;               // optimizer.py:88-90
         acc[1] += di * di + dout * dout;  // optimizer.py:93-96

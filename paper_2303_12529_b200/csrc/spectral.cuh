@@ -719,12 +719,12 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
 #endif
   extern __shared__ __align__(128) unsigned char smraw[];
   C* const base = reinterpret_cast<C*>(smraw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 3 * (size_t)op.bufE * sizeof(C));  // 3 ring + 1 side
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 3 * (size_t)op.bufE * sizeof(C));  // 3 ring + 2 side
   typename Op::State S{};
   if ((int)blockIdx.x >= op.nitems) return;
   const bool leader = threadIdx.x == 0;
   if (leader) {
-    for (int i = 0; i < 4; ++i) tma::mbar_init(&bar[i], 1);
+    for (int i = 0; i < 5; ++i) tma::mbar_init(&bar[i], 1);
     tma::fence_mbar_init();
   }
   __syncthreads();
@@ -738,6 +738,12 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
     op.load(nit, nst, base, &bar[0]);
   }
   advance(nit, nst);
+  // side operand of step q (kSideLoad ops): in the idle slot (q+2)%3, own
+  // mbarrier 3 + (q&1).  It is issued one step ahead, from inside step q-1
+  // once that step's last butterfly stage has read its slot (q-1)%3 ==
+  // (q+2)%3; only the first step of an item issues its own (the previous
+  // step's slot is then still busy with the item's closing transform).
+  bool side_pending = Op::kSideLoad;
   for (unsigned q = 0;; ++q) {
     const int slot = q % 3, nslot = (q + 1) % 3;
     C* const side = base + ((q + 2) % 3) * op.bufE;  // idle slot when the op stores nothing
@@ -747,15 +753,21 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
       op.load(nit, nst, base + nslot * op.bufE, &bar[nslot]);
     }
     if constexpr (Op::kSideLoad) {
-      if (leader) {
-        tma::mbar_expect_tx(&bar[3], op.load_bytes());
-        op.side_load(it, st, side, &bar[3]);
+      if (leader && side_pending) {
+        tma::mbar_expect_tx(&bar[3 + (q & 1)], op.load_bytes());
+        op.side_load(it, st, side, &bar[3 + (q & 1)]);
       }
     }
     tma::mbar_wait(&bar[slot], (q / 3) & 1);
     C* const cur = base + slot * op.bufE;
     if (st == 0) op.begin(S, it, cur);
-    op.step(S, it, st, cur, side, q);
+    if constexpr (Op::kSideLoad) {
+      const bool item_end = st == op.steps(it) - 1;
+      op.step_side(S, it, st, cur, side, q, bar, !item_end);
+      side_pending = item_end;
+    } else {
+      op.step(S, it, st, cur, side, q);
+    }
     if (Op::kStores) {
       tma::fence_async_smem();
       __syncthreads();
@@ -968,8 +980,9 @@ template <typename R> struct TA1Op : OpBase {
 
 // TA2: V_set = IFFT_y(sum_k w_k conj(H_k) FFT_y U_k).  U_k tiles arrive in the
 // ring; since the pass stores nothing per step, the ring's third slot is idle
-// and takes H_k of the current step (TMA, own mbarrier), which the last
-// butterfly stage reads from shared memory.
+// and holds H_k of the current step (TMA, own mbarrier), which the last
+// butterfly stage reads from shared memory.  H_k of step q+1 is requested as
+// soon as step q's last stage has read its operand slot, a full step ahead.
 template <typename R> struct TA2Op : A2Op<R> {
   using C = typename CT<R>::C;
   using State = typename A2Op<R>::State;
@@ -999,11 +1012,6 @@ template <typename R> struct TA2Op : A2Op<R> {
     col_boxes(x0, [&](int c0, int c1, int c2, int off) { tma::tensor_g2s(dst + off, m, c0, c1, c2, k, bar); });
   }
   LS_D void store(int, int, const C*) const {}
-  // the side-load mbarrier: 4th barrier behind the ring (k_pass_tma's layout)
-  LS_D uint64_t* side_bar() const {
-    extern __shared__ __align__(128) unsigned char smraw[];
-    return reinterpret_cast<uint64_t*>(smraw + 3 * (size_t)this->bufE * sizeof(C)) + 3;
-  }
   template <int LGN> struct F {
     const C* b;
     const C* h;     // H_k tile (natural [y][S]) in the side slot
@@ -1011,18 +1019,31 @@ template <typename R> struct TA2Op : A2Op<R> {
     unsigned parity;
     State& S;
     R w;
-    LS_D void pre_store() const { tma::mbar_wait(bar, parity); }
+    // next step's H_k, issued into this step's slot once every thread has
+    // read it (the engine's barrier after the last stage's loads)
+    const TA2Op* op;
+    int it, knext;
+    uint64_t* nbar;
+    bool issue;
+    LS_D void pre_store() const {
+      if (issue && threadIdx.x == 0) {
+        tma::mbar_expect_tx(nbar, op->load_bytes());
+        op->side_load(it, knext, const_cast<C*>(b), nbar);
+      }
+      tma::mbar_wait(bar, parity);
+    }
     template <int ST> LS_D C load(int seq, int j, int r, int) const { return b[nat_col<LGN, ST, C>(seq, j, r, 0)]; }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int slot) {
       S.acc[slot] = S.acc[slot] + cmulc(v, h[nat_col<LGN, ST, C>(seq, j, r, 0)]) * w;
     }
   };
-  LS_D void step(State& S, int it, int k, C* b, C* side, unsigned q) const {
+  LS_D void step_side(State& S, int it, int k, C* b, C* side, unsigned q, uint64_t* bars, bool issue_next) const {
     const Geo g = this->sh.gcol();
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       if constexpr (LGN > 0) {
-        F<LGN> f{b, side, side_bar(), q & 1u, S, this->a.w[it >> this->lgnt][k]};
+        F<LGN> f{b, side, &bars[3 + (q & 1u)], (q >> 1) & 1u, S, this->a.w[it >> this->lgnt][k],
+                 this, it, k + 1, &bars[3 + ((q + 1) & 1u)], issue_next};
         eng::run_fix<LGN, true, false>(g, b, this->tw, f);
       }
     });
@@ -1072,7 +1093,7 @@ int launch_op(Op& op, int threads, int extra_bufs, StopFlag stop, cudaStream_t s
 template <typename R, class Op>
 int launch_tma(Op& op, int threads, StopFlag stop, cudaStream_t s) {
   using C = typename CT<R>::C;
-  const size_t smem = 3 * (size_t)op.bufE * sizeof(C) + 4 * sizeof(uint64_t);
+  const size_t smem = 3 * (size_t)op.bufE * sizeof(C) + 5 * sizeof(uint64_t);
   if (smem > 227 * 1024) throw std::runtime_error("TMA pass needs more than 227 KB of shared memory");
   auto kern = k_pass_tma<R, Op>;
   static int per_sm = -1;

@@ -7,8 +7,14 @@ import numpy as np, torch
 import paper_2303_12529_b200 as b2
 from paper_2303_12529_b200 import _native as nv, inputs
 prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+side = int(sys.argv[2]) if len(sys.argv) > 2 else 2048       # 8192: configs[4] mosaic tile
+width = int(sys.argv[3]) if len(sys.argv) > 3 else side       # < side: a strip window
 nv.set_precision(prec)
-clip = inputs.iccad_like_clip(seed=0)
+if side == 2048:
+    clip = inputs.iccad_like_clip(seed=0)
+else:
+    g = side // 2048
+    clip = np.ascontiguousarray(inputs.mosaic_tile(range(g * g), grid=(g, g))[:, :width])
 (fc, fw), (dc, dw) = inputs.synthetic_kernel_arrays(35, 24, 4)
 focus = b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(fc, fw)], "focus")
 defocus = b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(dc, dw)], "defocus")
@@ -22,4 +28,5 @@ ms = (ctypes.c_double * 8)()
 nv.check(L.lsopc_session_time_passes(sess, 3, ms))
 nv.check(L.lsopc_session_time_passes(sess, 10, ms))
 names = ["mask", "F1", "F2", "resist", "A1", "A2", "A3", "ls"]
-print(" ".join(f"{n}={ms[i]*1e3:.0f}us" for i, n in enumerate(names)), f"total={sum(ms)*1e3:.0f}us")
+print(f"{prec} {clip.shape[0]}x{clip.shape[1]}:", " ".join(f"{n}={ms[i]*1e3:.0f}us" for i, n in enumerate(names)),
+      f"total={sum(ms)*1e3:.0f}us")
