@@ -650,6 +650,13 @@ template <typename R> struct A3Op : OpBase {
 // ===========================================================================
 // TMA variants of the four kernel-looping passes.
 //
+// Measured on B200: the TMA engine's cost grows with the number of box rows,
+// so a whole-tile column item (one contiguous 64 KB block) is fetched by one
+// 1-D bulk copy rather than 2048 tensor-box rows of 32 B (F1 661 -> 581 us,
+// A2 653 -> 566 us).  Row items keep natural [row][x] boxes: a row-group box
+// (4 rows of a tile = 128 B per box row) needs a swizzled [tile][row] shared
+// layout whose half-warp reads conflict 2-way, which measured slower.
+//
 // Same arithmetic as F1Op / F2Op / A1Op / A2Op; operands arrive by TMA
 // (1-D bulk copies of contiguous rows / tiles, 4-D tensor copies for the
 // column-tiled fields) into a 3-slot ring guarded by mbarriers, and the
@@ -815,6 +822,11 @@ template <typename R> struct TF1Op : OpBase {
   LS_D unsigned load_bytes() const { return (unsigned)((sh.H << sh.lgS) * sizeof(C)); }
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
     const int set = it >> lgnt, x0 = (it & ((1 << lgnt) - 1)) << sh.lgS;
+    if (spec_lgw == sh.lgS) {  // the item is one whole tile: a contiguous block, one 1-D bulk copy
+      tma::bulk_g2s(dst, a.spec[set] + (size_t)k * sh.H * sh.W + ((size_t)(x0 >> spec_lgw) * sh.H << spec_lgw),
+                    load_bytes(), bar);
+      return;
+    }
     const CUtensorMap* m = set ? &tmap_spec1 : &tmap_spec;
     col_boxes(x0, k, spec_lgw, [&](int c0, int c1, int c2, int kk, int off) {
       tma::tensor_g2s(dst + off, m, c0, c1, c2, kk, bar);
@@ -1000,14 +1012,25 @@ template <typename R> struct TA2Op : A2Op<R> {
     const int rows = this->sh.H < 256 ? this->sh.H : 256;
     for (int b = 0; b * rows < this->sh.H; ++b) fn((x0 & (w - 1)) * ew, x0 >> u_lgw, b * rows, b * rows * S);
   }
+  // whole-tile items are contiguous blocks: one 1-D bulk copy each
+  LS_D size_t tile_off(int x0) const { return (size_t)(x0 >> u_lgw) * this->sh.H << u_lgw; }
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
     const int set = it >> this->lgnt, x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
+    if (u_lgw == this->sh.lgS) {
+      tma::bulk_g2s(dst, this->a.T[0] + (size_t)(k + koff[set]) * this->sh.H * this->sh.W + tile_off(x0),
+                    load_bytes(), bar);
+      return;
+    }
     col_boxes(x0, [&](int c0, int c1, int c2, int off) {
       tma::tensor_g2s(dst + off, &tmap_U, c0, c1, c2, k + koff[set], bar);
     });
   }
   LS_D void side_load(int it, int k, C* dst, uint64_t* bar) const {
     const int set = it >> this->lgnt, x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
+    if (u_lgw == this->sh.lgS) {
+      tma::bulk_g2s(dst, this->a.spec[set] + (size_t)k * this->sh.H * this->sh.W + tile_off(x0), load_bytes(), bar);
+      return;
+    }
     const CUtensorMap* m = set ? &tmap_spec1 : &tmap_spec;
     col_boxes(x0, [&](int c0, int c1, int c2, int off) { tma::tensor_g2s(dst + off, m, c0, c1, c2, k, bar); });
   }
