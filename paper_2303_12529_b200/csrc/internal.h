@@ -73,9 +73,12 @@ void launch_adjoint(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop
 // out = scale * Re IFFT_x(V0 [+ V1]) (f64 row-major); with v_prev, per-CTA CG dot
 // partials dots[blk*2 + {0,1}] = {sum v (v - vp), sum vp^2}.  Returns the
 // number of partial blocks written (0 without v_prev).
+struct LoopTail;  // internal_ls.h
+// tail (nullable): the Polak-Ribiere control (after_grad) in the last CTA
 int launch_adjoint_finish(const Grid& g, const void* V0, const void* V1, double scale, double* out,
                           const double* v_prev, double* dots, StopFlag stop, cudaStream_t s, int ix0 = 0,
-                          int ix1 = 0);  // dots over columns [ix0, ix1) (0, 0: all)
+                          int ix1 = 0,  // dots over columns [ix0, ix1) (0, 0: all)
+                          const LoopTail* tail = nullptr);
 int finish_max_blocks();
 
 // ---- elementwise / reductions ---------------------------------------------------
@@ -90,7 +93,8 @@ void launch_resist(const Grid& g, const void* If, const void* Id, const uint8_t*
                    const double* target_f64, ResistParams p, void* wf, void* wd,
                    double* z_nom, double* z_in, double* z_out, uint8_t* h_nom,
                    uint8_t* h_in, uint8_t* h_out, double* partials, StopFlag stop,
-                   cudaStream_t s, int ix0 = 0, int ix1 = 0);  // losses over columns [ix0, ix1) (0, 0: all)
+                   cudaStream_t s, int ix0 = 0, int ix1 = 0,  // losses over columns [ix0, ix1) (0, 0: all)
+                   const LoopTail* tail = nullptr);  // after_forward fused into the DSO loop form
 // single-corner intensity output: out = max(dose * I, 0) (f64)
 void launch_scale_intensity(const Grid& g, const void* I, double dose, double* out, cudaStream_t s);
 // gate for a user-supplied print: w = scale * (z - zt) z (1 - z)   (element R)

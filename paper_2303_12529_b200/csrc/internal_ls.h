@@ -15,6 +15,7 @@ struct DevState {
   double vmax, gmax, dt;
   int stopped, improved, use_beta, streak, nhist, nonfinite_it;
   int it;  // index of the iteration in flight (advanced by the update's control kernel)
+  unsigned ticket[4];  // last-block tickets of the fused control tails (control.cuh), zero between launches
 };
 
 // Column ranges (window coordinates) of a strip of an oversized tile run on
@@ -32,6 +33,16 @@ struct LoopCfg {
   int stop_patience;
 };
 
+// Fused control tail of a producing kernel (control.cuh): its last block runs
+// the control body on the partials the kernel just wrote.  st == nullptr: none.
+struct LoopTail {
+  DevState* st;
+  double* hist;
+  LoopCfg c;
+  double eta;
+  int restart_every;
+};
+
 enum EwOp { EW_MASK = 1, EW_HEAVISIDE, EW_AXPBY, EW_SIGMOID, EW_HARD, EW_NEG, EW_CG, EW_MOTION, EW_EVOLVE, EW_AHF, EW_HYPOT };
 enum RdOp { RD_SUMSQDIFF = 1, RD_DOT, RD_DOTDIFF, RD_MAXABS, RD_COUNTNEQ8, RD_NONFINITE, RD_COUNTNEQ };
 
@@ -40,11 +51,14 @@ void launch_geometry(int H, int W, const double* phi, double* gx, double* gy, do
                      double* gxy, double* mag, cudaStream_t s);
 void launch_curvature(int H, int W, const double* phi, const double* m, double weight, double* out,
                       cudaStream_t s);
+// tail (nullable): run the CFL control (after_velocity) / the history record
+// (after_update) in the kernel's last block instead of a separate launch
 void launch_ls_velocity(int H, int W, const double* phi, const double* v, const double* dprev, const double* m,
-                        double weight, int use_curv, const DevState* st, double* d, double* u, double* gm,
-                        double* partials, Tile t, cudaStream_t s);
+                        double weight, int use_curv, DevState* st, double* d, double* u, double* gm,
+                        double* partials, Tile t, cudaStream_t s, const LoopTail* tail = nullptr);
 void launch_ls_update(int H, int W, double* phi, const double* u, const double* gm, double lo, double hi,
-                      const DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s);
+                      DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s,
+                      const LoopTail* tail = nullptr);
 void launch_dsn_init(size_t n, const float* phi_raw, const float* m_raw, double lo, double hi, double eps,
                      double* phi0, double* m, cudaStream_t s);
 // fixed-order reduction of nb blocks of nv partials (sum or max) into out[0..nv)

@@ -14,7 +14,10 @@
 // round-to-nearest intrinsics in the reference's evaluation order, so no FMA
 // contraction changes a bit: the stencil results are bit-identical to numpy.
 // |grad phi| reproduces glibc's hypot (the kernel numpy.hypot calls).
+#include <stdexcept>
+
 #include "common.cuh"
+#include "control.cuh"
 #include "internal_ls.h"
 
 namespace lsb {
@@ -121,41 +124,108 @@ k_curvature(int H, int W, const double* __restrict__ phi, const double* __restri
 
 // ---- loop kernels -------------------------------------------------------------
 
+// Stencil input of one pixel (levelset.py:112-118 operands + the loop fields)
+struct VelIn {
+  Geom g;
+  double v, dp, m;
+};
+
 // _step_fields (optimizer.py:180-194) + the update field of optimizer.py:262:
 //   d = -v (+ beta d_prev); v_total = d - kappa/(|grad phi| + 1e-8); u = -v_total |grad phi|
-__global__ void __launch_bounds__(kThreads)
+LS_D double vel_emit(const VelIn& a, int use_beta, double beta, int use_curv, bool have_m, double weight,
+                     double& gm_out, double& d_out) {
+  const double gm = np_hypot(a.g.gx, a.g.gy);
+  double d = -a.v;
+  if (use_beta) d = add(d, mul(beta, a.dp));
+  double vt = d;
+  if (use_curv) {
+    double k = curvature_of(a.g, weight);
+    if (have_m) k = mul(k, a.m);
+    vt = sub(d, dvd(k, add(gm, 1e-8)));
+  }
+  gm_out = gm;
+  d_out = d;
+  return vt;
+}
+
+// Two horizontally adjacent pixels (x even) per trip: the three stencil rows
+// are read as a 4-wide window (16 B loads for the centre pair), the loop
+// fields as double2, so each thread keeps enough bytes in flight; pairs that
+// touch a clamped column fall back to the per-pixel stencil.
+constexpr int kVelThreads = 192;  // 80 registers: four 6-warp blocks per SM keep kBlocks one wave
+__global__ void __launch_bounds__(kVelThreads, kBlocks / 148)
 k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __restrict__ v,
               const double* __restrict__ dprev, const double* __restrict__ m, double weight, int use_curv,
-              const DevState* st, double* d_out, double* u_out, double* gm_out, double* partials, Tile tl) {
+              DevState* st, double* d_out, double* u_out, double* gm_out, double* partials, Tile tl,
+              LoopTail tail) {
   __shared__ double red[64];
   if (st->stopped) return;
   const int use_beta = st->use_beta;
   const double beta = st->beta;
-  const size_t n = (size_t)H * W;
+  const size_t n2 = (size_t)H * W / 2;
   double mx[2] = {0.0, 0.0};  // max |v_total|, max |grad phi|
   const RowSplit rs = row_split(W);
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n2; q += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = 2 * q;
     const int y = (int)row_of(rs, i), x = (int)col_of(rs, i);
-    Geom g = geometry_at(phi, H, W, y, x, tl.xlo, tl.xhi);
-    double gm = np_hypot(g.gx, g.gy);
-    double d = -v[i];
-    if (use_beta) d = add(d, mul(beta, dprev[i]));
-    double vt = d;
-    if (use_curv) {
-      double k = curvature_of(g, weight);
-      if (m) k = mul(k, m[i]);
-      vt = sub(d, dvd(k, add(gm, 1e-8)));
-    }
-    d_out[i] = d;
-    if (gm_out) {  // modulation_search form: keep v_total and |grad phi| apart
-      u_out[i] = vt;
-      gm_out[i] = gm;
+    VelIn a[2];
+    if (x - 1 >= tl.xlo && x + 2 < tl.xhi) {
+      const int ys = y + 1 < H ? y + 1 : H - 1, yn = y > 0 ? y - 1 : 0;
+      const double* r = phi + (size_t)y * W + x;
+      const double* rS = phi + (size_t)ys * W + x;
+      const double* rN = phi + (size_t)yn * W + x;
+      const double2 c0 = *reinterpret_cast<const double2*>(r), s0 = *reinterpret_cast<const double2*>(rS),
+                    n0 = *reinterpret_cast<const double2*>(rN);
+      const double cw = r[-1], ce = r[2], sw = rS[-1], se = rS[2], nw = rN[-1], ne = rN[2];
+      // window columns x-1, x, x+1, x+2 of rows y, y+1 (s), y-1 (n)
+      const double R0[4] = {cw, c0.x, c0.y, ce}, S0[4] = {sw, s0.x, s0.y, se}, N0[4] = {nw, n0.x, n0.y, ne};
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        Geom& g = a[e].g;
+        const double c = R0[1 + e], ee = R0[2 + e], w = R0[e], s = S0[1 + e], nn = N0[1 + e];
+        g.gx = mul(0.5, sub(ee, w));
+        g.gy = mul(0.5, sub(s, nn));
+        g.gxx = sub(add(ee, w), mul(2.0, c));
+        g.gyy = sub(add(s, nn), mul(2.0, c));
+        g.gxy = mul(0.25, sub(sub(S0[2 + e], S0[e]), sub(N0[2 + e], N0[e])));
+      }
     } else {
-      u_out[i] = mul(-vt, gm);
+      a[0].g = geometry_at(phi, H, W, y, x, tl.xlo, tl.xhi);
+      a[1].g = geometry_at(phi, H, W, y, x + 1, tl.xlo, tl.xhi);
     }
-    if (x >= tl.ix0 && x < tl.ix1) {
-      mx[0] = fmax(mx[0], fabs(vt));
-      mx[1] = fmax(mx[1], gm);
+    const double2 vv = *reinterpret_cast<const double2*>(v + i);
+    a[0].v = vv.x;
+    a[1].v = vv.y;
+    if (use_beta) {
+      const double2 t = *reinterpret_cast<const double2*>(dprev + i);
+      a[0].dp = t.x;
+      a[1].dp = t.y;
+    } else {
+      a[0].dp = a[1].dp = 0.0;
+    }
+    if (m) {
+      const double2 t = *reinterpret_cast<const double2*>(m + i);
+      a[0].m = t.x;
+      a[1].m = t.y;
+    } else {
+      a[0].m = a[1].m = 1.0;
+    }
+    double vt[2], gm[2], d[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) vt[e] = vel_emit(a[e], use_beta, beta, use_curv, m != nullptr, weight, gm[e], d[e]);
+    *reinterpret_cast<double2*>(d_out + i) = make_double2(d[0], d[1]);
+    if (gm_out) {  // modulation_search form: keep v_total and |grad phi| apart
+      *reinterpret_cast<double2*>(u_out + i) = make_double2(vt[0], vt[1]);
+      *reinterpret_cast<double2*>(gm_out + i) = make_double2(gm[0], gm[1]);
+    } else {
+      *reinterpret_cast<double2*>(u_out + i) = make_double2(mul(-vt[0], gm[0]), mul(-vt[1], gm[1]));
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (x + e >= tl.ix0 && x + e < tl.ix1) {
+        mx[0] = fmax(mx[0], fabs(vt[e]));
+        mx[1] = fmax(mx[1], gm[e]);
+      }
     }
   }
   block_max<2>(mx, red);
@@ -163,143 +233,96 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
     partials[2 * blockIdx.x] = mx[0];
     partials[2 * blockIdx.x + 1] = mx[1];
   }
+  if (tail.st && last_block(&tail.st->ticket[2], red)) {
+    after_velocity_body(partials, gridDim.x, tail.eta, tail.st, tail.hist, red);
+    release_ticket(&tail.st->ticket[2]);
+  }
 }
 
-// optimizer.py:266-268: phi <- clip(phi + dt * u, D_l, D_u); next mask = [phi <= 0]
+// optimizer.py:266-268: phi <- clip(phi + dt * u, D_l, D_u); next mask = [phi <= 0].
+// Four pixels per trip (16 B loads); a group that straddles the strip
+// interior's edge takes the per-pixel path (halo pixels are left untouched).
 __global__ void __launch_bounds__(kThreads)
 k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const double* __restrict__ gm, double lo,
-            double hi, const DevState* st, uint8_t* mask, double* partials, Tile tl) {
+            double hi, DevState* st, uint8_t* mask, double* partials, Tile tl, LoopTail tail) {
   __shared__ double red[32];
   if (st->stopped) return;
   const double dt = st->dt;
-  const size_t n = (size_t)H * W;
+  const size_t n4 = (size_t)H * W / 4;
   double mx[1] = {0.0};
   const RowSplit rs = row_split(W);
   const bool whole = tl.ix0 <= 0 && tl.ix1 >= W;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int x = whole ? 0 : (int)col_of(rs, i);
-    if (x < tl.ix0 || x >= tl.ix1) continue;  // strip halo: owned by a neighbour rank
-    double step, p;
+  auto one = [&](double ph, double uu, double gg, double& step) {
     if (gm) {  // optimizer.py:329: phi - dt * v_total * grad_mag
-      step = mul(mul(dt, u[i]), gm[i]);
-      p = fmin(fmax(sub(phi[i], step), lo), hi);
-    } else {   // optimizer.py:262,266: phi + dt * (-v_total * grad_mag)
-      step = mul(dt, u[i]);
-      p = fmin(fmax(add(phi[i], step), lo), hi);
+      step = mul(mul(dt, uu), gg);
+      return fmin(fmax(sub(ph, step), lo), hi);
     }
-    phi[i] = p;
-    mask[i] = p <= 0.0;
-    mx[0] = fmax(mx[0], fabs(step));
+    step = mul(dt, uu);  // optimizer.py:262,266: phi + dt * (-v_total * grad_mag)
+    return fmin(fmax(add(ph, step), lo), hi);
+  };
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n4; q += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = 4 * q;
+    const int x = whole ? 0 : (int)col_of(rs, i);
+    if (whole || (x >= tl.ix0 && x + 4 <= tl.ix1)) {
+      const double2 p0 = *reinterpret_cast<const double2*>(phi + i), p1 = *reinterpret_cast<const double2*>(phi + i + 2);
+      const double2 u0 = *reinterpret_cast<const double2*>(u + i), u1 = *reinterpret_cast<const double2*>(u + i + 2);
+      double2 g0 = make_double2(0.0, 0.0), g1 = g0;
+      if (gm) {
+        g0 = *reinterpret_cast<const double2*>(gm + i);
+        g1 = *reinterpret_cast<const double2*>(gm + i + 2);
+      }
+      double s0, s1, s2, s3;
+      const double q0 = one(p0.x, u0.x, g0.x, s0), q1 = one(p0.y, u0.y, g0.y, s1), q2 = one(p1.x, u1.x, g1.x, s2),
+                   q3 = one(p1.y, u1.y, g1.y, s3);
+      *reinterpret_cast<double2*>(phi + i) = make_double2(q0, q1);
+      *reinterpret_cast<double2*>(phi + i + 2) = make_double2(q2, q3);
+      *reinterpret_cast<uchar4*>(mask + i) = make_uchar4(q0 <= 0.0, q1 <= 0.0, q2 <= 0.0, q3 <= 0.0);
+      mx[0] = fmax(fmax(fmax(mx[0], fabs(s0)), fmax(fabs(s1), fabs(s2))), fabs(s3));
+    } else {
+      for (int e = 0; e < 4; ++e) {
+        if (x + e < tl.ix0 || x + e >= tl.ix1) continue;  // strip halo: owned by a neighbour rank
+        double step;
+        const double p = one(phi[i + e], u[i + e], gm ? gm[i + e] : 0.0, step);
+        phi[i + e] = p;
+        mask[i + e] = p <= 0.0;
+        mx[0] = fmax(mx[0], fabs(step));
+      }
+    }
   }
   block_max<1>(mx, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = mx[0];
+  if (tail.st && last_block(&tail.st->ticket[3], red)) {
+    after_update_body(partials, gridDim.x, tail.st, tail.hist, red);
+    release_ticket(&tail.st->ticket[3]);
+  }
 }
 
 __global__ void k_copy_best(size_t n, const double* __restrict__ phi, double* best, const DevState* st) {
   if (!st->improved) return;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    best[i] = phi[i];
+  const size_t n2 = n / 2;  // 16 B copies, odd tail below
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x)
+    reinterpret_cast<double2*>(best)[i] = reinterpret_cast<const double2*>(phi)[i];
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) best[n - 1] = phi[n - 1];
 }
 
-// fixed-order reduction of nb partial pairs by one block
-template <int NV, bool MAX>
-LS_D void reduce_partials(const double* part, int nb, double (&out)[NV], double* red) {
-  double acc[NV];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) acc[j] = 0.0;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) acc[j] = MAX ? fmax(acc[j], part[NV * b + j]) : acc[j] + part[NV * b + j];
-  }
-  if (MAX) block_max<NV>(acc, red);
-  else block_sum<NV>(acc, red);
-#pragma unroll
-  for (int j = 0; j < NV; ++j) out[j] = acc[j];
-}
+// ---- loop control: single-block kernels (strip phases, API); the DSO graph
+// runs the same bodies as fused tails of their producers (control.cuh)
 
-// optimizer.py:238-251: loss, best iterate, patience
 __global__ void k_after_forward(const double* part, int nb, LoopCfg c, DevState* st, double* hist) {
   __shared__ double red[64];
-  if (st->stopped) return;
-  double l[2];
-  reduce_partials<2, false>(part, nb, l, red);
-  if (threadIdx.x != 0) return;
-  const double l_ilt = l[0], l_pvb = l[1];
-  const double l_dso = c.alpha * l_ilt + c.beta * l_pvb;
-  st->l_ilt = l_ilt;
-  st->l_pvb = l_pvb;
-  st->l_dso = l_dso;
-  st->improved = 0;
-  if (!isfinite(l_dso)) {
-    st->nonfinite_it = st->it;
-    st->stopped = 1;
-    return;
-  }
-  double rel;
-  if (l_dso < st->best) {
-    rel = isfinite(st->best) ? (st->best - l_dso) / st->best : CUDART_INF;
-    st->best = l_dso;
-    st->improved = 1;
-  } else {
-    rel = 0.0;
-  }
-  st->streak = rel < c.stop_rel_tol ? st->streak + 1 : 0;
-  if (st->streak >= c.stop_patience) {
-    double* h = hist + 7 * st->nhist;
-    h[0] = l_ilt; h[1] = l_pvb; h[2] = l_dso; h[3] = 0.0; h[4] = 0.0; h[5] = 0.0; h[6] = 0.0;
-    st->nhist += 1;
-    st->stopped = 1;
-  }
+  after_forward_body(part, nb, c, st, hist, red);
 }
-
-// optimizer.py:154-169,253: Polak-Ribiere beta with restart
 __global__ void k_after_grad(const double* dots, int nb, int restart_every, DevState* st) {
   __shared__ double red[64];
-  if (st->stopped) return;
-  const int restart = st->it == 0 || st->it % restart_every == 0;
-  double s[2] = {0.0, 0.0};
-  if (!restart) reduce_partials<2, false>(dots, nb, s, red);
-  if (threadIdx.x != 0) return;
-  st->use_beta = 0;
-  st->beta = 0.0;
-  if (restart || s[1] == 0.0) return;
-  double b = s[0] / s[1];
-  if (b <= 0.0) return;
-  st->beta = b;
-  st->use_beta = 1;
+  after_grad_body(dots, nb, restart_every, st, red);
 }
-
-// optimizer.py:143-151,257-261: dt = eta / max|v_total|
 __global__ void k_after_velocity(const double* part, int nb, double eta, DevState* st, double* hist) {
   __shared__ double red[64];
-  if (st->stopped) return;
-  double m[2];
-  reduce_partials<2, true>(part, nb, m, red);
-  if (threadIdx.x != 0) return;
-  st->vmax = m[0];
-  st->gmax = m[1];
-  if (m[0] == 0.0) {
-    double* h = hist + 7 * st->nhist;
-    h[0] = st->l_ilt; h[1] = st->l_pvb; h[2] = st->l_dso; h[3] = 0.0; h[4] = 0.0; h[5] = 0.0; h[6] = m[1];
-    st->nhist += 1;
-    st->stopped = 1;
-    return;
-  }
-  st->dt = eta / m[0];
+  after_velocity_body(part, nb, eta, st, hist, red);
 }
-
-// optimizer.py:262-265: history record of a completed step
 __global__ void k_after_update(const double* part, int nb, DevState* st, double* hist) {
   __shared__ double red[32];
-  if (st->stopped) return;
-  double m[1];
-  reduce_partials<1, true>(part, nb, m, red);
-  if (threadIdx.x != 0) return;
-  double* h = hist + 7 * st->nhist;
-  h[0] = st->l_ilt; h[1] = st->l_pvb; h[2] = st->l_dso; h[3] = st->dt; h[4] = st->vmax; h[5] = m[0];
-  h[6] = st->gmax;
-  st->nhist += 1;
-  st->it += 1;
+  after_update_body(part, nb, st, hist, red);
 }
 
 // ---- elementwise API operators -------------------------------------------------
@@ -396,13 +419,17 @@ void launch_curvature(int H, int W, const double* phi, const double* m, double w
   k_curvature<<<kBlocks, kThreads, 0, s>>>(H, W, phi, m, weight, out);
 }
 void launch_ls_velocity(int H, int W, const double* phi, const double* v, const double* dprev, const double* m,
-                        double weight, int use_curv, const DevState* st, double* d, double* u, double* gm,
-                        double* partials, Tile t, cudaStream_t s) {
-  k_ls_velocity<<<kBlocks, kThreads, 0, s>>>(H, W, phi, v, dprev, m, weight, use_curv, st, d, u, gm, partials, t);
+                        double weight, int use_curv, DevState* st, double* d, double* u, double* gm,
+                        double* partials, Tile t, cudaStream_t s, const LoopTail* tail) {
+  if (W % 4) throw std::invalid_argument("level-set loop kernels need a width divisible by 4");
+  k_ls_velocity<<<kBlocks, kVelThreads, 0, s>>>(H, W, phi, v, dprev, m, weight, use_curv, st, d, u, gm, partials, t,
+                                                tail ? *tail : LoopTail{});
 }
 void launch_ls_update(int H, int W, double* phi, const double* u, const double* gm, double lo, double hi,
-                      const DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s) {
-  k_ls_update<<<kBlocks, kThreads, 0, s>>>(H, W, phi, u, gm, lo, hi, st, mask, partials, t);
+                      DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s, const LoopTail* tail) {
+  if (W % 4) throw std::invalid_argument("level-set loop kernels need a width divisible by 4");
+  k_ls_update<<<kBlocks, kThreads, 0, s>>>(H, W, phi, u, gm, lo, hi, st, mask, partials, t,
+                                           tail ? *tail : LoopTail{});
 }
 void launch_copy_best(size_t n, const double* phi, double* best, const DevState* st, cudaStream_t s) {
   k_copy_best<<<kBlocks, kThreads, 0, s>>>(n, phi, best, st);

@@ -528,10 +528,12 @@ void enqueue_iteration(lsopc_session* ss, int par, cudaStream_t s, cudaEvent_t* 
   launch_f2(g, sets, 2, nullptr, stop, s);
   mark(3);
   ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
-  launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr, nullptr,
-                nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s);
   LoopCfg lc{c.alpha, c.beta, c.stop_rel_tol, c.stop_patience};
-  launch_after_forward(p->partials.as<double>(), reduce_blocks(), lc, st, ss->hist.as<double>(), s);
+  // each control step (loss/best/patience, CG beta, CFL step, record) runs in
+  // the last block of the kernel producing its partials (control.cuh)
+  const LoopTail tail{st, ss->hist.as<double>(), lc, c.eta, c.cg_restart_every};
+  launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr, nullptr,
+                nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s, 0, 0, &tail);
   launch_copy_best(n, ss->phi.as<double>(), ss->best.as<double>(), st, s);
   mark(4);
   // adjoint: U_k, then one frequency-domain accumulator per set and one inverse
@@ -539,19 +541,17 @@ void enqueue_iteration(lsopc_session* ss, int par, cudaStream_t s, cudaEvent_t* 
   mark(5);
   launch_a2(g, sets, 2, stop, s);
   mark(6);
-  int ndots = launch_adjoint_finish(g, p->V0.p, p->V1.p, 4.0 * c.sigma_z / (double)n, v, vprev,
-                                    ss->dots.as<double>(), stop, s);
+  launch_adjoint_finish(g, p->V0.p, p->V1.p, 4.0 * c.sigma_z / (double)n, v, vprev, ss->dots.as<double>(), stop, s,
+                        0, 0, &tail);
   mark(7);
-  launch_after_grad(ss->dots.as<double>(), ndots, c.cg_restart_every, st, s);
   // level-set step
   launch_ls_velocity(g.H, g.W, ss->phi.as<double>(), v, dprev, ss->have_mod ? ss->mod.as<double>() : nullptr,
                      c.curvature_weight, c.use_curvature, st, d, ss->u.as<double>(),
-                     c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), full_tile(g.W), s);
-  launch_after_velocity(ss->part_ls.as<double>(), ls_blocks(), c.eta, st, ss->hist.as<double>(), s);
+                     c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), full_tile(g.W), s,
+                     &tail);
   launch_ls_update(g.H, g.W, ss->phi.as<double>(), ss->u.as<double>(), c.update_form ? ss->gm.as<double>() : nullptr,
                    c.d_lower, c.d_upper, st, ss->mask.as<uint8_t>(),
-                   ss->part_up.as<double>(), full_tile(g.W), s);
-  launch_after_update(ss->part_up.as<double>(), ls_blocks(), st, ss->hist.as<double>(), s);
+                   ss->part_up.as<double>(), full_tile(g.W), s, &tail);
   mark(8);
   ck_launch("dso iteration");
 }

@@ -5,8 +5,12 @@
 //   corner doses (nominal / outer / inner)     litho.py:98-100,147-149
 //   ilt_loss / pvb_loss                        optimizer.py:88-96
 //   the adjoint gate (Z - Z_t) Z (1 - Z)       optimizer.py:109, 114-134
+#include <stdexcept>
+
 #include "common.cuh"
+#include "control.cuh"
 #include "internal.h"
+#include "internal_ls.h"
 
 namespace lsb {
 
@@ -18,6 +22,18 @@ constexpr int kRedBlocks = 148 * 4;
 constexpr int kRedThreads = 256;
 
 LS_D double sigmoid(double i, double i_th, double sz) { return 1.0 / (1.0 + exp(-sz * (i - i_th))); }
+
+// fp32 tier: Z and the gate Z (1 - Z) (Z - Z_t) in float from the float
+// intensity, 1 - Z formed as e / (1 + e) (no cancellation near Z = 1); the
+// loss sums accumulate in double
+struct ZF {
+  float z, omz;  // Z, 1 - Z
+};
+LS_D ZF sigmoid_f(float i, float i_th, float sz) {
+  const float e = expf(-sz * (i - i_th));
+  const float r = 1.0f / (1.0f + e);
+  return ZF{r, e * r};
+}
 
 template <typename R>
 __global__ void __launch_bounds__(kRedThreads)
@@ -43,6 +59,26 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
       if (h_in) h_in[i] = i_in >= p.i_th;
     }
     if (!z_nom && !wf && !partials) continue;
+    if constexpr (sizeof(R) == 4) {
+      if (!z_nom && have_t) {  // the DSO loop's form: losses + gates only
+        const float fth = (float)p.i_th, fsz = (float)p.sigma_z;
+        const ZF n = sigmoid_f((float)i_nom, fth, fsz), o = sigmoid_f((float)i_out, fth, fsz),
+                 d = sigmoid_f((float)i_in, fth, fsz);
+        const float zt = tu8 ? (float)tu8[i] : (float)tf[i];
+        const float dn = n.z - zt, di = d.z - zt, dout = o.z - zt;
+        const int x = whole ? ix0 : (int)col_of(rs, i);
+        if (x >= ix0 && x < ix1) {
+          acc[0] += (double)dn * dn;
+          acc[1] += (double)di * di + (double)dout * dout;
+        }
+        if (wf) {
+          const float gn = dn * n.z * n.omz, go = dout * o.z * o.omz, gi = di * d.z * d.omz;
+          wf[i] = (R)(p.alpha * gn + p.beta * 1.02 * go);
+          wd[i] = (R)(p.beta * 0.98 * gi);
+        }
+        continue;
+      }
+    }
     double zn = sigmoid(i_nom, p.i_th, p.sigma_z);
     double zo = sigmoid(i_out, p.i_th, p.sigma_z);
     double zi = sigmoid(i_in, p.i_th, p.sigma_z);
@@ -78,6 +114,109 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
   }
 }
 
+// The DSO loop's form of k_resist (losses + gates, no Z / print outputs),
+// four consecutive pixels per thread with 16 B loads and stores: the
+// pointwise pass is latency-bound unless each thread keeps several vector
+// loads in flight.  Arithmetic per pixel is exactly k_resist's.
+LS_D void ld4(const float* p, size_t i, float (&o)[4]) {
+  const float4 t = *reinterpret_cast<const float4*>(p + i);
+  o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+}
+LS_D void ld4(const double* p, size_t i, double (&o)[4]) {
+  const double2 a = *reinterpret_cast<const double2*>(p + i), b = *reinterpret_cast<const double2*>(p + i + 2);
+  o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+}
+LS_D void st4(float* p, size_t i, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(p + i) = make_float4(v[0], v[1], v[2], v[3]);
+}
+LS_D void st4(double* p, size_t i, const double (&v)[4]) {
+  *reinterpret_cast<double2*>(p + i) = make_double2(v[0], v[1]);
+  *reinterpret_cast<double2*>(p + i + 2) = make_double2(v[2], v[3]);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kRedThreads)
+k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, const uint8_t* __restrict__ tu8,
+              const double* __restrict__ tf, ResistParams p, R* wf, R* wd, double* partials, StopFlag stop, int W,
+              int ix0, int ix1, LoopTail tail) {
+  __shared__ double red[64];
+  if (stop && *stop) return;
+  double acc[2] = {0.0, 0.0};
+  const RowSplit rs = row_split(W);
+  const bool whole = ix0 <= 0 && ix1 >= W;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n4; g += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = 4 * g;
+    R sf[4], sd[4] = {(R)0, (R)0, (R)0, (R)0};
+    R zt[4];
+    ld4(If, i, sf);
+    if (Id) ld4(Id, i, sd);
+    if (tu8) {  // binary targets: a select, not an int->float conversion
+      const uchar4 t = *reinterpret_cast<const uchar4*>(tu8 + i);
+      const unsigned char tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) zt[e] = tv[e] == 0 ? (R)0 : tv[e] == 1 ? (R)1 : (R)tv[e];
+    } else {
+      double t[4];
+      ld4(tf, i, t);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) zt[e] = (R)t[e];
+    }
+    const int x0 = whole ? ix0 : (int)col_of(rs, i);
+    R gf[4], gd[4];
+    if constexpr (sizeof(R) == 4) {
+      // all-float arithmetic (conversions run on the narrow XU pipe); each
+      // 4-pixel group's loss terms are summed in float, then in double
+      const float fth = (float)p.i_th, fsz = (float)p.sigma_z, fa = (float)p.alpha, fbo = (float)(p.beta * 1.02),
+                  fbi = (float)(p.beta * 0.98);
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const ZF zn = sigmoid_f(fmaxf(sf[e], 0.f), fth, fsz), zo = sigmoid_f(fmaxf(1.02f * sf[e], 0.f), fth, fsz),
+                 zi = sigmoid_f(Id ? fmaxf(0.98f * sd[e], 0.f) : 0.f, fth, fsz);
+        const float t = (float)zt[e];
+        const float dn = zn.z - t, di = zi.z - t, dout = zo.z - t;
+        if (whole || (x0 + e >= ix0 && x0 + e < ix1)) {
+          s0 += dn * dn;
+          s1 += di * di + dout * dout;
+        }
+        gf[e] = fa * (dn * zn.z * zn.omz) + fbo * (dout * zo.z * zo.omz);
+        gd[e] = fbi * (di * zi.z * zi.omz);
+      }
+      acc[0] += (double)s0;
+      acc[1] += (double)s1;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double i_nom = fmax(1.0 * (double)sf[e], 0.0);
+        const double i_out = fmax(1.02 * (double)sf[e], 0.0);
+        const double i_in = Id ? fmax(0.98 * (double)sd[e], 0.0) : 0.0;
+        const double zn = sigmoid(i_nom, p.i_th, p.sigma_z), zo = sigmoid(i_out, p.i_th, p.sigma_z),
+                     zi = sigmoid(i_in, p.i_th, p.sigma_z);
+        const double dn = zn - zt[e], di = zi - zt[e], dout = zo - zt[e];
+        if (whole || (x0 + e >= ix0 && x0 + e < ix1)) {
+          acc[0] += dn * dn;
+          acc[1] += di * di + dout * dout;
+        }
+        gf[e] = (R)(p.alpha * (dn * zn * (1.0 - zn)) + p.beta * 1.02 * (dout * zo * (1.0 - zo)));
+        gd[e] = (R)(p.beta * 0.98 * (di * zi * (1.0 - zi)));
+      }
+    }
+    if (wf) {
+      st4(wf, i, gf);
+      st4(wd, i, gd);
+    }
+  }
+  block_sum<2>(acc, red);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = acc[0];
+    partials[2 * blockIdx.x + 1] = acc[1];
+  }
+  if (tail.st && last_block(&tail.st->ticket[0], red)) {
+    after_forward_body(partials, gridDim.x, tail.c, tail.st, tail.hist, red);
+    release_ticket(&tail.st->ticket[0]);
+  }
+}
+
 template <typename R>
 __global__ void k_scale_intensity(size_t n, const R* __restrict__ I, double dose, double* out) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -100,8 +239,22 @@ int reduce_blocks() { return kRedBlocks; }
 void launch_resist(const Grid& g, const void* If, const void* Id, const uint8_t* tu8, const double* tf,
                    ResistParams p, void* wf, void* wd, double* z_nom, double* z_in, double* z_out,
                    uint8_t* h_nom, uint8_t* h_in, uint8_t* h_out, double* partials, StopFlag stop,
-                   cudaStream_t s, int ix0, int ix1) {
+                   cudaStream_t s, int ix0, int ix1, const LoopTail* tail) {
   if (ix1 <= 0) ix1 = g.W;
+  const LoopTail tl = tail ? *tail : LoopTail{};
+  const bool loop_form = !z_nom && !h_nom && (tu8 || tf) && partials && g.n() % 4 == 0 && g.W % 4 == 0;
+  if (loop_form) {
+    if (g.prec == F64)
+      k_resist_loop<double><<<kRedBlocks, kRedThreads, 0, s>>>(
+          g.n() / 4, static_cast<const double*>(If), static_cast<const double*>(Id), tu8, tf, p,
+          static_cast<double*>(wf), static_cast<double*>(wd), partials, stop, g.W, ix0, ix1, tl);
+    else
+      k_resist_loop<float><<<kRedBlocks, kRedThreads, 0, s>>>(
+          g.n() / 4, static_cast<const float*>(If), static_cast<const float*>(Id), tu8, tf, p,
+          static_cast<float*>(wf), static_cast<float*>(wd), partials, stop, g.W, ix0, ix1, tl);
+    return;
+  }
+  if (tail) throw std::invalid_argument("fused loop control needs the DSO loop form of the resist pass");
   if (g.prec == F64)
     k_resist<double><<<kRedBlocks, kRedThreads, 0, s>>>(
         g.n(), static_cast<const double*>(If), static_cast<const double*>(Id), tu8, tf, p,

@@ -29,8 +29,10 @@
 // adjoint-spectrum accumulators stay on chip.
 #pragma once
 #include "common.cuh"
+#include "control.cuh"
 #include "engine.cuh"
 #include "internal.h"
+#include "internal_ls.h"
 #include "tma.cuh"
 
 #include <cudaTypedefs.h>
@@ -636,6 +638,7 @@ template <typename R> struct A3Op : OpBase {
       eng::run_fix<LGN, false, true>(g, b, tw, f);
     });
   }
+  LoopTail tail;  // st != nullptr: Polak-Ribiere control in the last CTA (control.cuh)
   LS_D void finish(State& S, double* red) const {
     if (!vp) return;
     __syncthreads();
@@ -643,6 +646,10 @@ template <typename R> struct A3Op : OpBase {
     if (threadIdx.x == 0) {
       dots[2 * blockIdx.x] = S.acc[0];
       dots[2 * blockIdx.x + 1] = S.acc[1];
+    }
+    if (tail.st && last_block(&tail.st->ticket[1], red)) {
+      after_grad_body(dots, gridDim.x, tail.restart_every, tail.st, red);
+      release_ticket(&tail.st->ticket[1]);
     }
   }
 };
@@ -1360,7 +1367,7 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
 
 template <typename R>
 int finish_impl(const Grid& g, const void* V0, const void* V1, double scale, double* out, const double* vp,
-                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1) {
+                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1, const LoopTail* tail) {
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   A3Op<R> a3;
@@ -1374,6 +1381,7 @@ int finish_impl(const Grid& g, const void* V0, const void* V1, double scale, dou
   a3.dots = dots;
   a3.ix0 = ix0;
   a3.ix1 = ix1 > 0 ? ix1 : g.W;
+  a3.tail = tail && vp ? *tail : LoopTail{};
   a3.bufE = row_bufE(sh);
   a3.nitems = g.H >> sh.lgR;
   int grid = launch_op<R>(a3, row_threads(sh), 0, stop, s, finish_max_blocks());
