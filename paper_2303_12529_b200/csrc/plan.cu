@@ -856,9 +856,9 @@ int lsopc_session_time_passes(lsopc_session* ss, int reps, double* ms_out) {
 
 int lsopc_session_launches_per_iter(const lsopc_session* ss) {
   if (!ss) return 0;
-  // mask rows+cols 2, F1 1, F2 1, resist 1, after_forward 1, copy_best 1, A1 1, A2 1,
-  // A3 1, after_grad 1, velocity+after 2, update+after 2
-  return 2 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 2 + 2;
+  // mask rows+cols 2, F1 1, F2 1, resist (+ loss control) 1, copy_best 1, A1 1, A2 1,
+  // A3 (+ CG control) 1, velocity (+ CFL control) 1, update (+ record) 1
+  return 2 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1;
 }
 
 int lsopc_optimize(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_kset* defocus, const uint8_t* target_dev,
