@@ -206,6 +206,11 @@ template <int LGN, int STRIDE, typename C, int LGT = lg_tile<C>()> LS_D size_t c
 template <int LGN, int STRIDE> LS_D size_t rm_row(int W, int y, int j, int r) {
   return (size_t)y * W + j + (size_t)r * STRIDE;
 }
+// row-major element (y = j + r*STRIDE, x)
+template <int LGN, int STRIDE> LS_D size_t rm_col(int W, int j, int r, int x) {
+  if constexpr (LGN > 0) return (size_t)(j + r * STRIDE) * W + x;
+  else return (size_t)j * W + x;
+}
 
 // ---------------------------------------------------------------------------
 // mask -> M~ = FFT_x(mask) (rows).  src: u8 mask, f64 mask, or f64 phi (mask = phi <= 0)
@@ -567,13 +572,15 @@ template <typename R> struct A2Op : OpBase {
       b[nat_col<LGN, ST, C>(seq, j, r, lgS)] = S.acc[slot];
     }
   };
+  // V_set is written row-major (once per item), so the A3 row pass reads
+  // whole contiguous row blocks
   template <int LGN> struct FOut {
     const C* b;
     C* out;
-    Lay L;
+    int W;
     int x0, lgS;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)]; }
-    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[ct_col<LGN, ST, C>(L, j, r, x0 + seq)] = v; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[rm_col<LGN, ST>(W, j, r, x0 + seq)] = v; }
   };
   LS_D void end(State& S, int it, C* b, C*) const {
     const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
@@ -582,7 +589,7 @@ template <typename R> struct A2Op : OpBase {
       constexpr int LGN = decltype(fx)::LGN;
       eng::for_last_slots<LGN, true, C>(g, PutAcc<LGN>{b, S, sh.lgS});
       __syncthreads();
-      FOut<LGN> f{b, a.V[set], sh.ct(), t << sh.lgS, sh.lgS};
+      FOut<LGN> f{b, a.V[set], sh.W, t << sh.lgS, sh.lgS};
       eng::run_fix<LGN, true, true>(g, b, tw, f);
     });
     __syncthreads();
@@ -603,11 +610,11 @@ template <typename R> struct A3Op : OpBase {
   double* dots;
   int ix0, ix1;  // dots over columns [ix0, ix1)
   LS_D void prefetch(int it, int, C* b, C*) const {
-    eng::gather_rect<sizeof(C)>(b, V0, sh.ct(), it << sh.lgR, sh.lgR, 0, sh.lgW);
+    eng::gather_rect<sizeof(C)>(b, V0, sh.rm(), it << sh.lgR, sh.lgR, 0, sh.lgW);
   }
   template <int LGN> struct F {
     const C* b;
-    const C* v1;  // second accumulator, read directly (column-tiled)
+    const C* v1;  // second accumulator, read directly (row-major, coalesced)
     Lay L;
     double scale;
     double* out;
@@ -616,7 +623,8 @@ template <typename R> struct A3Op : OpBase {
     int y0, lgn, W, ix0, ix1;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const C x = b[nat_row<LGN, ST>(seq, j, r, lgn)];
-      return v1 ? x + __ldg(&v1[ct_row<LGN, ST, C>(L, y0 + seq, j, r)]) : x;
+      if constexpr (LGN > 0) return v1 ? x + __ldg(&v1[rm_row<LGN, ST>(W, y0 + seq, j, r)]) : x;
+      else return v1 ? x + __ldg(&v1[(size_t)(y0 + seq) * W + j]) : x;
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
       const size_t p = rm_row<LGN, ST>(W, y0 + seq, j, r);
@@ -634,7 +642,7 @@ template <typename R> struct A3Op : OpBase {
     const Geo g = sh.grow();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      F<LGN> f{b, V1, sh.ct(), scale, out, vp, S, it << sh.lgR, sh.lgW, sh.W, ix0, ix1};
+      F<LGN> f{b, V1, sh.rm(), scale, out, vp, S, it << sh.lgR, sh.lgW, sh.W, ix0, ix1};
       eng::run_fix<LGN, false, true>(g, b, tw, f);
     });
   }
