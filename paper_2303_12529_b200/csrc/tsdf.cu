@@ -5,11 +5,14 @@
 //
 // Separable exact EDT.  Column pass: vertical distance g to the nearest
 // feature pixel in the same column, computed by (column, row-segment) threads
-// and a fix-up across segments.  Row pass: Felzenszwalb & Huttenlocher lower
-// envelope of the parabolas (x - q)^2 + g(q)^2, one thread per (row,
-// feature), with parabola intersections compared as exact integer fractions.  Squared distances are
-// exact integers, so phi = -/+ (sqrt(d2) - 0.5) is bit-identical to the
-// reference.
+// and a fix-up across segments.  Row pass: per pixel, the minimum of
+// (x - q)^2 + g(q)^2 by an outward scan bounded by the best value so far and
+// by the truncation (k_edt_rows_scan).  Squared distances are exact
+// integers, so phi = -/+ (sqrt(d2) - 0.5) is bit-identical to the reference.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+
 #include "common.cuh"
 #include "internal_ls.h"
 
@@ -74,83 +77,78 @@ __global__ void k_edt_cols_fix(int H, int W, const int2* __restrict__ seg, int* 
   }
 }
 
-// Row pass.  One thread per (row, feature) pair; the envelope stack lives in
-// global scratch laid out [k][thread] (coalesced across the warp, L1/L2
-// resident).  Parabola p_q(x) = (x - q)^2 + g(q)^2; the intersection of p_a
-// and p_b (a < b) is at x = num / den with num = key(b) - key(a),
-// key(q) = q^2 + g(q)^2, den = 2 (b - a) > 0; intersections are compared as
-// exact 64-bit integer fractions (no floating-point division).
-__global__ void __launch_bounds__(128) k_edt_rows(int H, int W, const uint8_t* __restrict__ mask,
-                                                 const int* __restrict__ g, int* stack, double d_upper,
-                                                 double d_lower, double* phi) {
-  const int nt = 2 * H;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nt) return;
-  const int f = t / H, y = t % H;
-  int* V = stack;                   // column q
-  int* G = stack + (size_t)W * nt;  // g(q)
-#define SV(i) V[(size_t)(i) * nt + t]
-#define SG(i) G[(size_t)(i) * nt + t]
-  const int* gr = g + (size_t)f * H * W + (size_t)y * W;
-  auto key = [](long long q, long long gq) { return gq * gq + q * q; };
-  int k = -1;
-  long long kt = 0, kp = 0;  // keys of the stack top and of the entry below it
-  long long vt = 0, vp = 0;
-  for (int q = 0; q < W; ++q) {
-    const int gq = gr[q];
-    if (gq >= kInf) continue;
-    const long long kq = key(q, gq);
-    // pop while s(top, q) <= z(top): (kq - kt)(vt - vp) <= (kt - kp)(q - vt)
-    while (k >= 1 && (kq - kt) * (vt - vp) <= (kt - kp) * (q - vt)) {
-      --k;
-      vt = vp;
-      kt = kp;
-      if (k >= 1) {
-        vp = SV(k - 1);
-        kp = key(vp, SG(k - 1));
-      }
+// Row pass.  d2(x) = min over q of (x - q)^2 + g(q)^2.  Each pixel scans
+// outward from q = x: a candidate at offset t costs at least t^2, so the scan
+// stops as soon as t^2 reaches the best d2 found so far (then d2 is exact), or
+// reaches `clip`, a squared distance beyond which the truncated value is the
+// clip bound whatever the exact distance is.  Work per pixel is therefore
+// min(distance, clip distance); with the TSDF's truncation (D_u = 900,
+// D_l = -100) every pixel of a 2048^2 clip finishes in a few hundred steps,
+// and one block per row keeps all SMs busy (the Felzenszwalb-Huttenlocher
+// envelope it replaces is sequential along the row: one thread per row).
+// The row's g values (both features) are staged in shared memory; all
+// comparisons are on exact integers.
+template <typename D>  // D: unsigned when every squared distance fits (sides <= 32768), else long long
+__global__ void __launch_bounds__(256) k_edt_rows_scan(int H, int W, const uint8_t* __restrict__ mask,
+                                                      const int* __restrict__ g, D clip_dark, D clip_lit,
+                                                      double d_upper, double d_lower, double* phi, int staged) {
+  extern __shared__ int sg[];  // [2][W] when staged
+  const int y = blockIdx.x;
+  const int* g1 = g + (size_t)y * W;                   // f = 0: distance to the nearest lit pixel
+  const int* g0 = g + (size_t)H * W + (size_t)y * W;   // f = 1: distance to the nearest dark pixel
+  if (staged) {
+    for (int i = threadIdx.x; i < W; i += blockDim.x) {
+      sg[i] = g1[i];
+      sg[W + i] = g0[i];
     }
-    ++k;
-    SV(k) = q;
-    SG(k) = gq;
-    vp = vt;
-    kp = kt;
-    vt = q;
-    kt = kq;
+    __syncthreads();
+    g1 = sg;
+    g0 = sg + W;
   }
-  // k >= 0: the feature set is non-empty (uniform masks are rejected upstream)
-  int j = 0;
-  long long vj = SV(0), kj = key(vj, SG(0));
-  long long vn = k >= 1 ? SV(1) : 0, kn = k >= 1 ? key(vn, SG(1)) : 0;
-  for (int x = 0; x < W; ++x) {
-    // advance while the next parabola's start z(j+1) = (kn - kj) / (2 (vn - vj)) < x
-    while (j < k && kn - kj < (long long)x * 2 * (vn - vj)) {
-      ++j;
-      vj = vn;
-      kj = kn;
-      if (j < k) {
-        vn = SV(j + 1);
-        kn = key(vn, SG(j + 1));
-      }
-    }
-    const long long d2 = (x - vj) * (x - vj) + (kj - vj * vj);
+  constexpr D kBig = sizeof(D) == 4 ? (D)UINT_MAX : (D)LLONG_MAX;
+  auto sq = [](int v) -> D { return v < kInf ? (D)v * (D)v : kBig; };  // columns without a feature: none
+  for (int x = threadIdx.x; x < W; x += blockDim.x) {
     const size_t p = (size_t)y * W + x;
     const bool lit = mask[p] != 0;
-    // feature 0 = lit pixels -> distances for dark pixels; feature 1 -> lit pixels
-    if ((f == 0) != lit) {
-      const double d = sqrt((double)d2);
-      const double val = lit ? -(d - 0.5) : d - 0.5;
-      phi[p] = fmin(fmax(val, d_lower), d_upper);
+    // lit pixels take the distance to the nearest dark pixel, dark pixels to the nearest lit one
+    const int* G = lit ? g0 : g1;
+    const D clip = lit ? clip_lit : clip_dark;
+    D best = sq(G[x]);
+    D lim = best < clip ? best : clip;
+    const int reach = max(x, W - 1 - x);
+    D t2 = 1;
+    for (int t = 1; t <= reach && t2 < lim; ++t, t2 += 2 * t - 1) {
+      const int l = G[max(x - t, 0)], r = G[min(x + t, W - 1)];  // clamped reads, masked below
+      const D cl = x - t >= 0 ? sq(l) : kBig, cr = x + t < W ? sq(r) : kBig;
+      const D c = cl < cr ? cl : cr;
+      if (c < kBig && t2 + c < best) best = t2 + c;
+      lim = best < clip ? best : clip;
     }
+    double val;
+    if (best >= clip) {
+      val = lit ? d_lower : d_upper;  // truncated whatever the exact distance
+    } else {
+      const double d = sqrt((double)best);
+      val = lit ? -(d - 0.5) : d - 0.5;
+      val = fmin(fmax(val, d_lower), d_upper);
+    }
+    phi[p] = val;
   }
-#undef SV
-#undef SG
+}
+
+// smallest squared integer distance from which the truncated value is the
+// clip bound with margin: d >= bound + 1 (the value is d - 0.5 past the bound
+// by at least 0.5, so rounding of sqrt cannot matter)
+long long clip_d2(double bound) {
+  const double d = std::fabs(bound) + 1.0;
+  const double d2 = std::ceil(d * d);
+  return d2 >= 4.0e18 ? (long long)4.0e18 : (long long)d2;
 }
 
 }  // namespace
 
 size_t tsdf_scratch_i32(int H, int W) {
-  return (size_t)2 * H * W + (size_t)2 * kSegs * W * 2 + (size_t)2 * W * 2 * H;  // g, segments, stacks
+  return (size_t)2 * H * W + (size_t)2 * kSegs * W * 2;  // g, segments
 }
 size_t tsdf_scratch_f64(int H, int W) { return 1; }
 
@@ -162,8 +160,21 @@ void launch_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_low
   const dim3 cg((W + 127) / 128, kSegs);
   k_edt_cols_local<<<cg, 128, 0, s>>>(H, W, mask, g, seg);
   k_edt_cols_fix<<<cg, 128, 0, s>>>(H, W, seg, g);
-  int* stack = si + (size_t)2 * H * W + (size_t)2 * kSegs * W * 2;
-  k_edt_rows<<<(2 * H + 127) / 128, 128, 0, s>>>(H, W, mask, g, stack, d_upper, d_lower, phi);
+  // dark pixels: value d - 0.5 reaches D_u; lit pixels: -(d - 0.5) reaches D_l
+  const long long clip_dark = clip_d2(d_upper + 0.5), clip_lit = clip_d2(0.5 - d_lower);
+  const size_t sm = (size_t)2 * W * sizeof(int);
+  const int staged = sm <= 200 * 1024;
+  const bool narrow = H <= 32768 && W <= 32768;  // t^2 + g^2 < 2^31
+  auto run = [&](auto zero) {
+    using D = decltype(zero);
+    auto k = k_edt_rows_scan<D>;
+    if (staged && sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const long long big = sizeof(D) == 4 ? (long long)UINT_MAX : LLONG_MAX;
+    k<<<H, 256, staged ? sm : 0, s>>>(H, W, mask, g, (D)std::min<long long>(clip_dark, big),
+                                     (D)std::min<long long>(clip_lit, big), d_upper, d_lower, phi, staged);
+  };
+  if (narrow) run(0u);
+  else run(0LL);
 }
 
 }  // namespace lsb
