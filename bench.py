@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--tile", type=int, default=8192, help="config 5 tile side, split over the ranks (0 = skip)")
     p.add_argument("--tile-iters", type=int, default=6)
     p.add_argument("--dsn-batch", type=int, default=16, help="config 4 batch (0 = skip)")
+    p.add_argument("--modsearch", type=int, default=41,
+                   help="modulation_search candidates on one 2048^2 target, sharded over the ranks (0 = skip)")
     return p.parse_args()
 
 
@@ -342,6 +344,24 @@ def b200_arm(args, world, rank, local):
                    "note": "random-init two-branch UNet (bf16) -> fused clip + AHF -> DSO per clip to the stop "
                            "rule (configs[3]); per rank"}
 
+    # ---- modulation_search, candidates sharded ---------
+    modsearch = None
+    if args.modsearch > 0 and not args.no_solve:
+        cfg_m = b2.OptConfig(precision=args.precision)
+        tgt = inputs.iccad_like_clip(seed=0)
+        phi_gt = b2.tsdf_from_mask(tgt)
+        parallel.modulation_search_sharded(phi_gt, tgt, focus, defocus, cfg_m, num_samples=4,
+                                           eval_steps=10, synchronize=torch.cuda.synchronize)  # warm-up
+        rm, secs = parallel.modulation_search_sharded(phi_gt, tgt, focus, defocus, cfg_m,
+                                                      num_samples=args.modsearch, eval_steps=10,
+                                                      synchronize=torch.cuda.synchronize)
+        modsearch = {"candidates": args.modsearch, "eval_steps": 10, "seconds": round(secs, 3),
+                     "candidates_per_s": round(args.modsearch / secs, 2),
+                     "best_delta_h": float(rm.best_delta_h),
+                     "note": f"modulation_search(TSDF of iccad_like_clip(0), 41 shifts of the gate, 10 "
+                             f"curvature-on iterations each, device-side final L_DSO); candidates round-robin "
+                             f"over {world} GPU(s), 2 streams per GPU, one all-gather of the scores"}
+
     # ---- config 5: one oversized tile split into strips over the ranks -------
     tile = None
     if args.tile > 0 and not args.no_solve:
@@ -408,6 +428,7 @@ def b200_arm(args, world, rank, local):
         "batch": batch,
         "tile": tile,
         "instant_opc": instant,
+        "modulation_search": modsearch,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

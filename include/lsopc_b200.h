@@ -173,6 +173,12 @@ int lsopc_session_destroy(lsopc_session* s);
 /* Current (not best) phi of the session, f64 [H][W]; used by
  * modulation_search (optimizer.py:317-336), which scores the last iterate. */
 int lsopc_session_phi(lsopc_session* s, double* phi_dev);
+/* L_ilt, L_pvb and L_DSO = alpha L_ilt + beta L_pvb of the session's current
+ * phi: _forward_losses(mask_from_phi(phi)) (optimizer.py:172-177), computed
+ * on the device whether or not the loop has stopped (modulation_search's
+ * candidate score, optimizer.py:334-336).  Synchronises the session stream;
+ * any output pointer may be NULL. */
+int lsopc_session_losses(lsopc_session* s, double* l_ilt, double* l_pvb, double* l_dso);
 /* Number of kernel launches one DSO iteration enqueues (bench accounting). */
 int lsopc_session_launches_per_iter(const lsopc_session* s);
 

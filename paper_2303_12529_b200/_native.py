@@ -74,6 +74,7 @@ _SIGS = {
     "lsopc_session_poll": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "lsopc_session_finish": (_I, [_P, _P, _P, _P, ctypes.POINTER(LsopcResult)]),
     "lsopc_session_phi": (_I, [_P, _P]),
+    "lsopc_session_losses": (_I, [_P, _P, _P, _P]),
     "lsopc_session_destroy": (_I, [_P]),
     "lsopc_session_launches_per_iter": (_I, [_P]),
     "lsopc_fracture": (_I, [_I, _I, _P, _P, _Z, ctypes.POINTER(_Z)]),

@@ -784,6 +784,33 @@ int lsopc_session_phi(lsopc_session* ss, double* phi_dev) {
   });
 }
 
+int lsopc_session_losses(lsopc_session* ss, double* l_ilt, double* l_pvb, double* l_dso) {
+  return guarded([&] {
+    if (!ss) throw Error(LSOPC_EINVAL, "null session");
+    lsopc_plan* p = ss->plan;
+    const Grid& g = p->g;
+    const lsopc_config& c = ss->cfg;
+    cudaStream_t s = ss->s;
+    SpecSet sets[2] = {spec_set(p, ss->focus, 0, 0), spec_set(p, ss->defocus, 1, ss->focus->nk)};
+    // _forward_losses on mask_from_phi(phi) (optimizer.py:172-177, 334-336); not gated by the stop flag
+    launch_mask_fft(g, nullptr, nullptr, ss->phi.as<double>(), p->mhat.p, p->scratch.p, nullptr, s);
+    launch_f1(g, p->mhat.p, sets, 2, nullptr, s);
+    launch_f2(g, sets, 2, nullptr, nullptr, s);
+    ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
+    ss->scalars.ensure(8 * sizeof(double));
+    double* sc = ss->scalars.as<double>();
+    launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, nullptr, nullptr, nullptr, nullptr,
+                  nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), nullptr, s);
+    launch_reduce_partials(p->partials.as<double>(), reduce_blocks(), 2, 0, sc, s);
+    double h[2];
+    ck(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, s), "memcpy");
+    ck(cudaStreamSynchronize(s), "sync");
+    if (l_ilt) *l_ilt = h[0];
+    if (l_pvb) *l_pvb = h[1];
+    if (l_dso) *l_dso = c.alpha * h[0] + c.beta * h[1];
+  });
+}
+
 int lsopc_session_destroy(lsopc_session* ss) {
   return guarded([&] {
     if (!ss) return;

@@ -349,42 +349,67 @@ class ModulationSearchResult:
     candidates: list = field(default_factory=list)
 
 
+def modulation_offsets(num_samples):
+    """Candidate shifts delta_h of modulation_search (optimizer.py:306-307)."""
+    if num_samples < 1:
+        raise ValueError("num_samples must be >= 1")
+    return [0.0] if num_samples == 1 else list(np.linspace(-20.0, 20.0, num_samples))
+
+
+def modulation_eval_cfg(cfg):
+    """The search's evaluation config: curvature on (optimizer.py:308)."""
+    return OptConfig(**{**cfg.__dict__, "use_curvature": True})
+
+
+def modulation_score(phi_gt, target, focus_kernels, defocus_kernels, eval_cfg, dh, eval_steps=10, resident=None):
+    """Final L_DSO of one candidate gate H(phi_gt + dh) (optimizer.py:312-336):
+    `eval_steps` device iterations from phi_gt with curvature gated by it
+    (CFL break, no patience rule), then the forward losses of the last
+    iterate, all on the device (lsopc_session_losses).  `resident` (a dict
+    owned by the caller, one per stream) keeps phi_gt and the target on the
+    device across candidates; the gate is formed there."""
+    import torch
+    key = (id(phi_gt), id(target))
+    target, _, fk, dk = _prepare(target, focus_kernels, defocus_kernels, eval_cfg, phi_gt, None)
+    res = resident if resident is not None else {}
+    if res.get("key") != key:
+        res.update(key=key, td=nv.to_dev(target, np.uint8), pd=nv.to_dev(phi_gt.phi))
+    gate = ((res["pd"] + float(dh)) >= 0.0).to(torch.float64)  # levelset.py:142-144 on phi_gt + dh
+    c = _native_cfg(eval_cfg, max_iters=eval_steps, stop_patience=2**31 - 1, use_curvature=True, update_form=1)
+    L = nv.lib()
+    sess = ctypes.c_void_p()
+    nv.check(L.lsopc_session_create(fk.plan.handle, fk.handle, dk.handle, nv.ptr(res["td"]), nv.ptr(res["pd"]),
+                                    nv.ptr(gate), ctypes.byref(c), nv.stream(), ctypes.byref(sess)))
+    try:
+        if eval_steps > 0:
+            nv.check(L.lsopc_session_enqueue(sess, eval_steps))
+        l_dso = ctypes.c_double()
+        nv.check(L.lsopc_session_losses(sess, None, None, ctypes.byref(l_dso)))
+    finally:
+        L.lsopc_session_destroy(sess)
+    return float(l_dso.value)
+
+
+def modulation_pick(phi_gt, candidates, gate=None):
+    """Best candidate, ties on smallest |dh| then dh (optimizer.py:338-341);
+    m_gt = gate(phi_gt + best_dh), the device Heaviside by default."""
+    best_loss = min(l for _, l in candidates)
+    tied = [dh for dh, l in candidates if l == best_loss]
+    best_dh = min(tied, key=lambda d: (abs(d), d))
+    m_gt = (gate or heaviside)(phi_gt.phi + best_dh).astype(np.float64)
+    return ModulationSearchResult(m_gt, best_dh, list(candidates))
+
+
 def modulation_search(phi_gt, target, focus_kernels, defocus_kernels, cfg, num_samples=41,
                       eval_steps=10):
     """Exhaustive curvature-gate search (optimizer.py:294-341): each candidate
     gate H(phi_gt + dh) is scored by L_DSO after `eval_steps` device
-    iterations with curvature on; ties break on smallest |dh|, then dh."""
-    if num_samples < 1:
-        raise ValueError("num_samples must be >= 1")
+    iterations with curvature on; ties break on smallest |dh|, then dh.
+    `parallel.modulation_search_sharded` spreads the candidates over GPUs."""
+    offsets = modulation_offsets(num_samples)
     target = _check_target(target)
-    offsets = [0.0] if num_samples == 1 else list(np.linspace(-20.0, 20.0, num_samples))
-    eval_cfg = OptConfig(**{**cfg.__dict__, "use_curvature": True})
-    _, _, fk, dk = _prepare(target, focus_kernels, defocus_kernels, eval_cfg, phi_gt, None)
-    shape = target.shape
-    td = nv.to_dev(target, np.uint8)
-    pd = nv.to_dev(phi_gt.phi)
-    c = _native_cfg(eval_cfg, max_iters=eval_steps, stop_patience=2**31 - 1, use_curvature=True,
-                    update_form=1)
-    candidates, gates = [], {}
-    phi_out = nv.empty(shape, np.float64)
-    for dh in offsets:
-        gate = heaviside(phi_gt.phi + dh).astype(np.float64)
-        gates[dh] = gate
-        sess = ctypes.c_void_p()
-        nv.check(nv.lib().lsopc_session_create(fk.plan.handle, fk.handle, dk.handle, nv.ptr(td),
-                                               nv.ptr(pd), nv.ptr(nv.to_dev(gate)), ctypes.byref(c),
-                                               nv.stream(), ctypes.byref(sess)))
-        try:
-            nv.check(nv.lib().lsopc_session_enqueue(sess, eval_steps))
-            nv.check(nv.lib().lsopc_session_phi(sess, nv.ptr(phi_out)))
-            stopped = ctypes.c_int()
-            nv.check(nv.lib().lsopc_session_poll(sess, ctypes.byref(stopped), None))
-        finally:
-            nv.lib().lsopc_session_destroy(sess)
-        mask = mask_from_phi(nv.to_host(phi_out)).astype(np.float64)
-        _, _, _, l_final = _forward_losses(mask, target, focus_kernels, defocus_kernels, eval_cfg)
-        candidates.append((dh, l_final))
-    best_loss = min(l for _, l in candidates)
-    tied = [dh for dh, l in candidates if l == best_loss]
-    best_dh = min(tied, key=lambda d: (abs(d), d))
-    return ModulationSearchResult(gates[best_dh], best_dh, candidates)
+    eval_cfg = modulation_eval_cfg(cfg)
+    resident = {}
+    candidates = [(dh, modulation_score(phi_gt, target, focus_kernels, defocus_kernels, eval_cfg, dh, eval_steps,
+                                        resident)) for dh in offsets]
+    return modulation_pick(phi_gt, candidates)

@@ -129,6 +129,73 @@ def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, sol
     return gather_records(records, group), seconds
 
 
+def modulation_search_sharded(phi_gt, target, focus_kernels, defocus_kernels, cfg, num_samples=41,
+                              eval_steps=10, group=None, lanes=2, scorer=None, synchronize=None):
+    """`modulation_search` (optimizer.py:294-341) with its candidates spread
+    over the ranks: candidate i runs on rank i mod world,
+    `lanes` streams per GPU score alternate candidates, and one all-gather of
+    the (index, delta_h, L_DSO) triples gives every rank the full candidate
+    list, from which each picks the same winner with the reference's
+    tie-break.  Returns (ModulationSearchResult, seconds = max over ranks).
+
+    `scorer(dh) -> L_DSO` replaces the device evaluation (tests inject a stub).
+    """
+    import torch.distributed as dist
+
+    from .optimizer import (_check_target, modulation_eval_cfg, modulation_offsets, modulation_pick,
+                            modulation_score)
+    rank, world = world_info(group)
+    offsets = modulation_offsets(num_samples)
+    target = _check_target(target)
+    eval_cfg = modulation_eval_cfg(cfg)
+    mine = [(i, offsets[i]) for i in shard(len(offsets), rank, world)]
+    if synchronize:
+        synchronize()
+    t0 = time.perf_counter()
+    scored = []
+    if scorer is not None:
+        scored = [(i, dh, float(scorer(dh))) for i, dh in mine]
+    else:
+        import threading
+        from concurrent.futures import ThreadPoolExecutor
+
+        import torch
+
+        from . import _native as nv
+        lock = threading.Lock()
+        dev = torch.cuda.current_device()
+
+        def worker(lane, items):
+            nv.set_lane(lane)
+            torch.cuda.set_device(dev)
+            stream = torch.cuda.Stream()
+            resident = {}  # phi_gt and the target stay on the device for this lane's candidates
+            with torch.cuda.stream(stream):
+                for i, dh in items:
+                    loss = modulation_score(phi_gt, target, focus_kernels, defocus_kernels, eval_cfg, dh, eval_steps,
+                                            resident)
+                    with lock:
+                        scored.append((i, dh, loss))
+            stream.synchronize()
+
+        with ThreadPoolExecutor(max_workers=lanes) as pool:
+            for f in [pool.submit(worker, l, mine[l::lanes]) for l in range(lanes)]:
+                f.result()
+    if synchronize:
+        synchronize()
+    seconds = max_over_ranks(time.perf_counter() - t0, group)
+    if dist.is_available() and dist.is_initialized():
+        parts = [None] * dist.get_world_size(group)
+        dist.all_gather_object(parts, scored, group=group)
+        scored = [t for part in parts for t in part]
+    scored.sort(key=lambda t: t[0])
+    if [t[0] for t in scored] != list(range(len(offsets))):
+        raise RuntimeError("modulation_search_sharded: candidate set incomplete after the gather")
+    # with a stub scorer (CPU tests) the winning gate is formed on the host
+    gate = (lambda p: p >= 0.0) if scorer is not None else None
+    return modulation_pick(phi_gt, [(dh, l) for _, dh, l in scored], gate), seconds
+
+
 def warm_lanes(target, focus_kernels, defocus_kernels, cfg, lanes=2):
     """Solve `target` once on every lane (no collectives), so the lanes'
     spectra, work buffers and captured iteration graphs exist before timing."""

@@ -6,7 +6,8 @@ Run in the build container only (the reference is not on the GPU box):
     NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py /tmp/refpkg [--big]
 
 Outputs `tests/golden/*.npz`.  Each fixture records the reference function it
-came from.  `--big` adds the 2048^2 / N_k=24 full-size samples (~3 min).
+came from.  `--big` adds the 2048^2 / N_k=24 full-size samples (~3 min);
+`--only modsearch` regenerates just `modsearch.npz`.
 """
 
 import hashlib
@@ -21,9 +22,25 @@ OUT = Path(__file__).resolve().parent
 def main():
     ref_path = sys.argv[1] if len(sys.argv) > 1 else "/tmp/refpkg"
     big = "--big" in sys.argv
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     sys.path.insert(0, ref_path)
     import lsopc
     from lsopc import levelset, litho, optimizer
+
+    # ---- modulation_search (optimizer.py:294-341) -------------------------------
+    ms = {}
+    f, d = litho.gen_synthetic_kernels(9, 2, seed=2)
+    t = np.zeros((64, 64), dtype=np.uint8)
+    t[16:40, 20:44] = 1
+    phi_gt = levelset.tsdf_from_mask(t)
+    for tag, cfg in (("default", optimizer.OptConfig()), ("nocurvw", optimizer.OptConfig(curvature_weight=0.0))):
+        r = optimizer.modulation_search(phi_gt, t, f, d, cfg, num_samples=5, eval_steps=3)
+        ms[f"{tag}_candidates"] = np.array([[dh, l] for dh, l in r.candidates])
+        ms[f"{tag}_best"] = np.array(r.best_delta_h)
+    ms["target"] = t
+    np.savez_compressed(OUT / "modsearch.npz", **ms)
+    if only == "modsearch":
+        return
 
     def kset_arrays(ks):
         return (np.stack([k.coeffs for k in ks.kernels]),

@@ -406,6 +406,27 @@ def test_modulation_search_small():
     assert r.best_delta_h == 0.0
 
 
+def test_modulation_search_sharded_matches_sequential():
+    """Candidates scored on two lanes (streams) give the sequential search's
+    losses bit for bit, and the oracle's within the fp64 tier's tolerance."""
+    from paper_2303_12529_b200 import parallel
+    nv.set_precision("fp64")
+    f, d, F, D = kernels(9, 2, 2)
+    target = np.zeros((64, 64), dtype=np.uint8)
+    target[16:40, 20:44] = 1
+    cfg = b2.OptConfig()
+    phi_gt = b2.tsdf_from_mask(target)
+    seq = b2.modulation_search(phi_gt, target, F, D, cfg, num_samples=5, eval_steps=3)
+    par, secs = parallel.modulation_search_sharded(phi_gt, target, F, D, cfg, num_samples=5, eval_steps=3, lanes=2)
+    assert par.candidates == seq.candidates
+    assert par.best_delta_h == seq.best_delta_h and np.array_equal(par.m_gt, seq.m_gt)
+    g = golden("modsearch")  # the reference's own candidates (tests/golden/make_golden.py)
+    assert np.array_equal(g["target"], target)
+    for (dh, l), (rdh, rl) in zip(seq.candidates, g["default_candidates"]):
+        assert dh == rdh and abs(l - rl) <= 1e-9 * abs(rl)
+    assert seq.best_delta_h == float(g["default_best"])
+
+
 @pytest.mark.gpu
 def test_reference_kernelset_objects_accepted():
     """Function-level drop-in: objects with the reference

@@ -107,3 +107,17 @@ def test_two_bar_layout_and_clip_generator():
     t = o.two_bar_512()
     assert t.sum() == 2 * 70 * 270
     assert [int(o.iccad_like_clip(s).sum()) for s in (0, 1, 2)] == [333562, 308514, 334395]
+
+
+def test_modulation_search_matches_reference():
+    """optimizer.py:294-341 restated; fixture from the real reference (make_golden.py)."""
+    g = golden("modsearch")
+    f, d = o.synthetic_kernels(9, 2, 2)
+    t = g["target"]
+    phi = o.tsdf(t)
+    r = o.modulation_search(phi, t, f, d, None, num_samples=5, eval_steps=3)
+    assert np.array_equal(np.array(r["candidates"]), g["default_candidates"])
+    assert r["best_delta_h"] == float(g["default_best"])
+    r = o.modulation_search(phi, t, f, d, o.Cfg(curvature_weight=0.0), num_samples=5, eval_steps=3)
+    assert np.array_equal(np.array(r["candidates"]), g["nocurvw_candidates"])
+    assert r["best_delta_h"] == float(g["nocurvw_best"])

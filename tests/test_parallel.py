@@ -88,3 +88,66 @@ def test_lazy_clips_are_deterministic():
     assert np.array_equal(a, c[0])
     with pytest.raises(IndexError):
         c[3]
+
+
+# ---- modulation_search candidates sharded over ranks ----------
+
+def _stub_score(dh):
+    # ties at dh = +-5 (loss 0): the reference's tie-break picks -5.0
+    return abs(abs(dh) - 5.0)
+
+
+def _ms_target():
+    t = np.zeros((8, 8), dtype=np.uint8)
+    t[2:6, 3:7] = 1
+    return t
+
+
+def _ms_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        phi = SimpleNamespace(phi=np.linspace(-3, 3, 64).reshape(8, 8))
+        cfg = SimpleNamespace(__dict__={})
+        from paper_2303_12529_b200 import OptConfig
+        r, secs = parallel.modulation_search_sharded(phi, _ms_target(), None, None, OptConfig(), num_samples=41,
+                                                     scorer=_stub_score)
+        q.put((rank, r.best_delta_h, r.candidates, r.m_gt.tolist(), secs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_modulation_search_sharded_single_process():
+    from paper_2303_12529_b200 import OptConfig
+    phi = SimpleNamespace(phi=np.linspace(-3, 3, 64).reshape(8, 8))
+    r, secs = parallel.modulation_search_sharded(phi, _ms_target(), None, None, OptConfig(), num_samples=41,
+                                                 scorer=_stub_score)
+    offsets = list(np.linspace(-20.0, 20.0, 41))
+    assert [dh for dh, _ in r.candidates] == offsets
+    assert [l for _, l in r.candidates] == [_stub_score(dh) for dh in offsets]
+    assert r.best_delta_h == -5.0
+    assert np.array_equal(r.m_gt, (phi.phi - 5.0 >= 0).astype(np.float64))
+    r1, _ = parallel.modulation_search_sharded(phi, _ms_target(), None, None, OptConfig(), num_samples=1,
+                                               scorer=_stub_score)
+    assert r1.best_delta_h == 0.0 and r1.candidates == [(0.0, 5.0)]
+
+
+def test_world2_gloo_modulation_search_agrees_on_every_rank():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ms_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    offsets = list(np.linspace(-20.0, 20.0, 41))
+    for rank, best, cands, m_gt, secs in out:
+        assert best == -5.0
+        assert [dh for dh, _ in cands] == offsets
+        assert [l for _, l in cands] == [_stub_score(dh) for dh in offsets]
+        assert secs >= 0.0
+    assert out[0][3] == out[1][3]
