@@ -715,18 +715,27 @@ inline CUtensorMap make_field_map(const TmaField& f, int H, int W, int NK, unsig
   return m;
 }
 
-// TMA path usable for this geometry (fast path, 16 B box rows, box <= 256)
-template <typename R> bool tma_ok(const Shape<R>& sh) {
-  using C = typename CT<R>::C;
+// TMA path usable for the row passes (F2, A1) / the column passes (F1, A2)
+// of this geometry: compile-time FFT geometry along that axis, and for
+// columns a slab of at least 16 B per tile row (a TMA box row).  The axes are
+// independent: an 8192-point column slab is 8 B wide (one complex64 column)
+// and stays on the cp.async path while the 8192-point rows stream by TMA.
+inline bool tma_disabled() {
   static const bool off = [] {
     const char* e = std::getenv("LSOPC_B200_NO_TMA");
     return e && e[0] == '1';
   }();
-  if (off || !sh.fast()) return false;
-  // the TMA op bodies exist only for the compile-time FFT geometry (eng::dispatch)
+  return off;
+}
+template <typename R> bool tma_ok_rows(const Shape<R>& sh) {
+  using C = typename CT<R>::C;
   constexpr int LGE = eng::lg_full<C>();
-  if (sh.lgH < eng::kFastMinLgn || sh.lgW < eng::kFastMinLgn || sh.lgS != LGE - sh.lgH || sh.lgR != LGE - sh.lgW)
-    return false;
+  return !tma_disabled() && sh.fast() && sh.lgW >= eng::kFastMinLgn && sh.lgR == LGE - sh.lgW;
+}
+template <typename R> bool tma_ok_cols(const Shape<R>& sh) {
+  using C = typename CT<R>::C;
+  constexpr int LGE = eng::lg_full<C>();
+  if (tma_disabled() || !sh.fast() || sh.lgH < eng::kFastMinLgn || sh.lgS != LGE - sh.lgH) return false;
   const int ew = sizeof(C) / 8;
   const int S = 1 << sh.lgS, w = 1 << lg_tile<C>();
   return std::min(S, w) * ew * 8 >= 16 && S % std::min(S, w) == 0;
@@ -1236,7 +1245,7 @@ void f1_impl(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, St
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
-  if (tma_ok(sh)) {
+  if (tma_ok_cols(sh)) {
     TF1Op<R> f1;
     f1.sh = sh;
     f1.a = a;
@@ -1279,7 +1288,7 @@ void f2_impl(const Grid& g, const SpecSet* sets, int nsets, double2* a0_out, Sto
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
-  if (tma_ok(sh)) {
+  if (tma_ok_rows(sh)) {
     TF2Op<R> f2;
     f2.sh = sh;
     f2.a = a;
@@ -1311,7 +1320,7 @@ void a1_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
-  if (tma_ok(sh)) {
+  if (tma_ok_rows(sh)) {
     TA1Op<R> a1;
     a1.sh = sh;
     a1.a = a;
@@ -1341,7 +1350,7 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
-  if (tma_ok(sh)) {
+  if (tma_ok_cols(sh)) {
     TA2Op<R> a2;
     a2.sh = sh;
     a2.a = a;
