@@ -77,20 +77,73 @@ Cand sweep_row(const int* heights, const uint8_t* mrow, int W, int y, std::vecto
 
 }  // namespace
 
-extern "C" int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* rects, size_t cap,
+extern "C" int lsopc_fracture(int H0, int W0, const uint8_t* mask_host, int32_t* rects, size_t cap,
                               size_t* count) {
-  if (H < 0 || W < 0 || !count) return LSOPC_EINVAL;
-  std::vector<uint8_t> m((size_t)H * W);
-  for (size_t i = 0; i < m.size(); ++i) m[i] = mask_host[i] != 0;
-  std::vector<int> hts((size_t)H * W, 0);
-  for (int y = 0; y < H; ++y)
-    for (int x = 0; x < W; ++x) {
-      size_t p = (size_t)y * W + x;
-      hts[p] = m[p] ? (y > 0 ? hts[p - W] : 0) + 1 : 0;
+  if (H0 < 0 || W0 < 0 || !count) return LSOPC_EINVAL;
+  // Work on the bounding box of the lit pixels: every rectangle lies inside
+  // it and the (area, top, left) order is translation invariant, so the
+  // rectangles are the reference's, offset by the box corner.
+  int y0 = H0, y1 = -1, x0 = W0, x1 = -1;
+  for (int y = 0; y < H0; ++y) {
+    const uint8_t* r = mask_host + (size_t)y * W0;
+    int x = 0, first = -1, last = -1;
+    for (; x + 8 <= W0; x += 8) {
+      uint64_t w8;
+      std::memcpy(&w8, r + x, 8);
+      if (w8) {
+        if (first < 0) first = x;
+        last = x + 7;
+      }
     }
+    for (; x < W0; ++x)
+      if (r[x]) {
+        if (first < 0) first = x;
+        last = x;
+      }
+    if (first < 0) continue;
+    while (!r[first]) ++first;
+    while (!r[last]) --last;
+    if (y0 == H0) y0 = y;
+    y1 = y;
+    x0 = first < x0 ? first : x0;
+    x1 = last > x1 ? last : x1;
+  }
+  if (y1 < 0) {
+    *count = 0;
+    return LSOPC_OK;
+  }
+  const int H = y1 - y0 + 1, W = x1 - x0 + 1;
+  const uint8_t* const mask_box = mask_host + (size_t)y0 * W0 + x0;  // row stride W0
+  thread_local std::vector<uint8_t> tls_m;
+  thread_local std::vector<int> tls_hts;
+  tls_m.resize((size_t)H * W);
+  tls_hts.resize((size_t)H * W);
+  uint8_t* const m = tls_m.data();  // raw pointers: no TLS or vector reloads in the loops
+  int* const hts = tls_hts.data();
+  // mask bytes and column run heights in one row-major pass (vectorisable:
+  // no dependence along a row), each row swept while it is still in cache
   std::vector<int> stack(W + 1);
   std::vector<Cand> rowbest(H);
-  for (int y = 0; y < H; ++y) rowbest[y] = sweep_row(&hts[(size_t)y * W], &m[(size_t)y * W], W, y, stack);
+  for (int y = 0; y < H; ++y) {
+    const uint8_t* __restrict__ src = mask_box + (size_t)y * W0;
+    uint8_t* __restrict__ mr = m + (size_t)y * W;
+    int* __restrict__ hr = hts + (size_t)y * W;
+    if (y == 0) {
+      for (int x = 0; x < W; ++x) {
+        const int v = src[x] != 0;
+        mr[x] = (uint8_t)v;
+        hr[x] = v;
+      }
+    } else {
+      const int* __restrict__ up = hr - W;
+      for (int x = 0; x < W; ++x) {
+        const int v = src[x] != 0;
+        mr[x] = (uint8_t)v;
+        hr[x] = v ? up[x] + 1 : 0;
+      }
+    }
+    rowbest[y] = sweep_row(hr, mr, W, y, stack);
+  }
   size_t k = 0;
   while (true) {
     Cand best;
@@ -98,8 +151,8 @@ extern "C" int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* r
       if (better(rowbest[y], best)) best = rowbest[y];
     if (best.area == 0) break;
     if (rects && k < cap) {
-      rects[4 * k] = best.x;
-      rects[4 * k + 1] = best.y;
+      rects[4 * k] = best.x + x0;
+      rects[4 * k + 1] = best.y + y0;
       rects[4 * k + 2] = best.w;
       rects[4 * k + 3] = best.h;
     }

@@ -300,25 +300,49 @@ def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, mod
     hist = np.zeros((cfg.max_iters + 1, 7))
     res = nv.LsopcResult()
     c = _native_cfg(cfg)
+    # the host array for the float64 phi is allocated and faulted in on a
+    # helper thread while the loop runs (the ctypes call releases the GIL)
+    phi_host = _tail_pool().submit(_touched_empty, shape)
     nv.check(nv.lib().lsopc_optimize(fk.plan.handle, fk.handle, dk.handle, nv.ptr(td), nv.ptr(p0),
                                      nv.ptr(mdv), ctypes.byref(c), nv.ptr(best), nv.ptr(fmask),
                                      hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res),
                                      nv.stream()))
     # device -> host through a pinned staging buffer; wall_time is taken before
-    # the shot count, as in the reference (optimizer.py:274-281)
+    # the shot count, as in the reference (optimizer.py:274-281).  The shot
+    # count (native, releases the GIL) of the final mask runs on a helper
+    # thread while the float64 phi is copied out.
     final_mask = nv.to_host(fmask)
+    shots = _tail_pool().submit(shot_count, final_mask)
     stage = nv.pinned_like(best)
     stage.copy_(best, non_blocking=True)
     nv.torch().cuda.current_stream().synchronize()
-    best_phi = stage.numpy().copy()
+    best_phi = phi_host.result()
+    np.copyto(best_phi, stage.numpy())
     wall = time.perf_counter() - t0
-    return final_mask, best_phi, (res.iters, res.l2, res.pvband), hist, wall
+    return final_mask, best_phi, (res.iters, res.l2, res.pvband), hist, wall, shots
+
+
+_TAIL = None
+
+
+def _touched_empty(shape):
+    a = np.empty(shape, dtype=np.float64)
+    a.fill(0.0)  # fault the pages in now, off the critical path
+    return a
+
+
+def _tail_pool():
+    global _TAIL
+    if _TAIL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _TAIL = ThreadPoolExecutor(max_workers=4, thread_name_prefix="lsopc-tail")
+    return _TAIL
 
 
 def _assemble(parts, cfg, phi0=None):
     """Host tail of `optimize`: shot count, history records, result."""
-    final_mask, best_phi, (iters, l2, pvb), hist, wall = parts
-    shots = shot_count(final_mask)
+    final_mask, best_phi, (iters, l2, pvb), hist, wall, shots = parts
+    shots = shots.result() if hasattr(shots, "result") else shot_count(final_mask)
     history = [IterationRecord(*(float(v) for v in row)) for row in hist[:iters]]
     bounds = (cfg.d_upper, cfg.d_lower)
     if phi0 is not None and not _is_device_tensor(phi0):
