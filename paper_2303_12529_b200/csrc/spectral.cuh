@@ -824,6 +824,92 @@ template <int LGN, int STRIDE, typename C, bool COLS> LS_D int nat_out(int seq, 
   else return nat_row<LGN, STRIDE>(seq, j, r, 0);
 }
 
+// TMaskRows: M~ = FFT_x(mask) (K1 rows).  The item's mask rows (u8, or f64
+// mask / phi) arrive by one 1-D bulk copy; the transform reads them from
+// shared memory in the first stage; M~ rows leave by per-row tensor boxes
+// into the column-tiled scratch (like TA1's U_k stores).
+template <typename R> struct TMaskRowsOp : OpBase {
+  using C = typename CT<R>::C;
+  using State = NoState;
+  static constexpr bool kStores = true;
+  static constexpr bool kSideLoad = false;
+  Shape<R> sh;
+  const void* src;
+  int kind;
+  const C* tw;
+  alignas(64) CUtensorMap tmap_out;  // M~ (one column-tiled field), row boxes
+  LS_D unsigned load_bytes() const { return (unsigned)((sh.W << sh.lgR) * (kind == SRC_U8 ? 1 : 8)); }
+  LS_D void load(int it, int, C* dst, uint64_t* bar) const {
+    const size_t off = ((size_t)it << sh.lgR) * sh.W * (kind == SRC_U8 ? 1 : 8);
+    tma::bulk_g2s(dst, static_cast<const unsigned char*>(src) + off, load_bytes(), bar);
+  }
+  LS_D void store(int it, int, const C* src_s) const {
+    constexpr int LGT = lg_tile<C>();
+    const int y0 = it << sh.lgR, tiles = sh.W >> LGT, bt = tiles < 256 ? tiles : 256;
+    for (int r = 0; r < (1 << sh.lgR); ++r)
+      for (int b = 0; b * bt < tiles; ++b)
+        tma::tensor_s2g(&tmap_out, 0, b * bt, y0 + r, 0, src_s + (r << sh.lgW) + ((b * bt) << LGT));
+  }
+  template <int LGN> struct F {
+    C* b;
+    int kind;
+    template <int ST> LS_D C load(int seq, int j, int r, int) const {
+      const int p = nat_row<LGN, ST>(seq, j, r, 0);
+      R m;
+      if (kind == SRC_U8) {
+        m = (R)reinterpret_cast<const unsigned char*>(b)[p];
+      } else {
+        const double v = reinterpret_cast<const double*>(b)[p];
+        m = kind == SRC_PHI ? (R)(v <= 0.0) : (R)v;
+      }
+      return cmk(m, (R)0);
+    }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, false>(seq, j, r)] = v; }
+  };
+  LS_D void step(State&, int, int, C* b, C*, unsigned) const {
+    const Geo g = sh.grow();
+    eng::dispatch<C>(g, true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) {
+        F<LGN> f{b, kind};
+        eng::run_fix<LGN, false, false>(g, b, tw, f);
+      }
+    });
+  }
+};
+
+// TCols: out = FFT_y(in) of whole-tile column items (K1 columns): one 1-D bulk
+// copy in, one out
+template <typename R> struct TColsOp : OpBase {
+  using C = typename CT<R>::C;
+  using State = NoState;
+  static constexpr bool kStores = true;
+  static constexpr bool kSideLoad = false;
+  Shape<R> sh;
+  const C* in;
+  C* out;
+  const C* tw;
+  LS_D unsigned load_bytes() const { return (unsigned)((sh.H << sh.lgS) * sizeof(C)); }
+  LS_D size_t tile_off(int it) const { return ((size_t)it << sh.lgS) * sh.H; }  // whole tiles: lgS == lgT
+  LS_D void load(int it, int, C* dst, uint64_t* bar) const { tma::bulk_g2s(dst, in + tile_off(it), load_bytes(), bar); }
+  LS_D void store(int it, int, const C* src_s) const { tma::bulk_s2g(out + tile_off(it), src_s, load_bytes()); }
+  template <int LGN> struct F {
+    C* b;
+    template <int ST> LS_D C load(int seq, int j, int r, int) const { return b[nat_col<LGN, ST, C>(seq, j, r, 0)]; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, true>(seq, j, r)] = v; }
+  };
+  LS_D void step(State&, int, int, C* b, C*, unsigned) const {
+    const Geo g = sh.gcol();
+    eng::dispatch<C>(g, true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) {
+        F<LGN> f{b};
+        eng::run_fix<LGN, true, false>(g, b, tw, f);
+      }
+    });
+  }
+};
+
 // TF1: T_k = IFFT_y(M^ . H_k)/(HW); H_k tile in by TMA, T_k slab out by TMA
 template <typename R> struct TF1Op : OpBase {
   using C = typename CT<R>::C;
@@ -1218,15 +1304,42 @@ void mask_fft_impl(const Grid& g, const void* src, int kind, void* mhat, void* s
                    cudaStream_t s) {
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
-  MaskRowsOp<R> mr;
-  mr.sh = sh;
-  mr.src = src;
-  mr.kind = kind;
-  mr.out = static_cast<C*>(scratch);
-  mr.tw = static_cast<const C*>(g.tw);
-  mr.bufE = row_bufE(sh);
-  mr.nitems = g.H >> sh.lgR;
-  launch_op<R>(mr, row_threads(sh), 0, stop, s);
+  const size_t src_bytes = ((size_t)1 << sh.lgR) * g.W * (kind == SRC_U8 ? 1 : 8);
+  if (tma_ok_rows(sh) && src_bytes % 16 == 0 && src_bytes <= (size_t)row_bufE(sh) * sizeof(C) &&
+      reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+    TMaskRowsOp<R> mr;
+    mr.sh = sh;
+    mr.src = src;
+    mr.kind = kind;
+    mr.tw = static_cast<const C*>(g.tw);
+    const int ew = sizeof(C) / 8, tiles = g.W >> sh.lgT;
+    mr.tmap_out = make_field_map(TmaField{scratch, sh.lgT, ew}, g.H, g.W, 1, (unsigned)((1 << sh.lgT) * ew),
+                                 (unsigned)std::min(tiles, 256), 1);
+    mr.bufE = tma_bufE<R>(row_bufE(sh));
+    mr.nitems = g.H >> sh.lgR;
+    launch_tma<R>(mr, row_threads(sh), stop, s);
+  } else {
+    MaskRowsOp<R> mr;
+    mr.sh = sh;
+    mr.src = src;
+    mr.kind = kind;
+    mr.out = static_cast<C*>(scratch);
+    mr.tw = static_cast<const C*>(g.tw);
+    mr.bufE = row_bufE(sh);
+    mr.nitems = g.H >> sh.lgR;
+    launch_op<R>(mr, row_threads(sh), 0, stop, s);
+  }
+  if (tma_ok_cols(sh) && sh.lgS == sh.lgT) {
+    TColsOp<R> mc;
+    mc.sh = sh;
+    mc.in = static_cast<const C*>(scratch);
+    mc.out = static_cast<C*>(mhat);
+    mc.tw = static_cast<const C*>(g.tw);
+    mc.bufE = tma_bufE<R>(col_bufE(sh));
+    mc.nitems = g.W >> sh.lgS;
+    launch_tma<R>(mc, col_threads(sh), stop, s);
+    return;
+  }
   ColsOp<R, R, false> mc;
   mc.sh = sh;
   mc.in = static_cast<const C*>(scratch);
