@@ -103,7 +103,7 @@ template <typename R, class Op>
 __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pass(Op op, StopFlag stop) {
   using C = typename CT<R>::C;
   constexpr int NB = Op::kStages;  // ring of stage buffers: prefetch distance NB - 1
-#if !defined(LSB_EXP_NOSTORE) && !defined(LSB_EXP_NOGATHER)
+#if !defined(LSB_EXP_NOSTORE) && !defined(LSB_EXP_NOGATHER) && !defined(LSB_EXP_NOTMA)
   if (stop && *stop) return;
 #endif
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -357,20 +357,23 @@ template <typename R> struct F1Op : OpBase {
     const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
     eng::gather_rect<sizeof(C)>(b, a.spec[set] + (size_t)k * fsz(), sh.ct(), 0, sh.lgH, t << sh.lgS, sh.lgS);
   }
+  // the item's M^ values, pre-multiplied by the IFFT's 1/(HW) (a power of
+  // two: exact), so the per-kernel product needs no extra scaling
   template <int LGN> struct LoadM {
     State& S;
     const C* mhat;
     Lay L;
     int x0;
+    R scale;
     template <int ST> LS_D void operator()(int seq, int j, int r, int slot) const {
-      S.mh[slot] = __ldg(&mhat[ct_col<LGN, ST, C>(L, j, r, x0 + seq)]);
+      S.mh[slot] = __ldg(&mhat[ct_col<LGN, ST, C>(L, j, r, x0 + seq)]) * scale;
     }
   };
   LS_D void begin(State& S, int it, C*) const {
     const int t = it & ((1 << lgnt) - 1);
     eng::dispatch<C>(sh.gcol(), sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      if constexpr (LGN > 0) eng::for_first_slots<LGN, true, C>(LoadM<LGN>{S, mhat, sh.ct(), t << sh.lgS});
+      if constexpr (LGN > 0) eng::for_first_slots<LGN, true, C>(LoadM<LGN>{S, mhat, sh.ct(), t << sh.lgS, scale});
     });
   }
   template <int LGN> struct F {
@@ -383,7 +386,7 @@ template <typename R> struct F1Op : OpBase {
     R scale;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const C x = b[nat_col<LGN, ST, C>(seq, j, r, lgS)];
-      if constexpr (LGN > 0) return cmul(S.mh[slot], x) * scale;
+      if constexpr (LGN > 0) return cmul(S.mh[slot], x);
       else return cmul(mhat[Lm.at(j, x0 + seq)], x) * scale;
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
@@ -745,7 +748,7 @@ template <typename R, class Op>
 __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pass_tma(const __grid_constant__ Op op,
                                                                                        StopFlag stop) {
   using C = typename CT<R>::C;
-#if !defined(LSB_EXP_NOSTORE) && !defined(LSB_EXP_NOGATHER)
+#if !defined(LSB_EXP_NOSTORE) && !defined(LSB_EXP_NOGATHER) && !defined(LSB_EXP_NOTMA)
   if (stop && *stop) return;
 #endif
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -765,8 +768,12 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
   int it = blockIdx.x, st = 0;
   int nit = it, nst = st;  // next step to load
   if (leader) {
+#ifdef LSB_EXP_NOTMA  // experiment builds only: on-chip work without data movement
+    tma::mbar_expect_tx(&bar[0], 0);
+#else
     tma::mbar_expect_tx(&bar[0], op.load_bytes());
     op.load(nit, nst, base, &bar[0]);
+#endif
   }
   advance(nit, nst);
   // side operand of step q (kSideLoad ops): in the idle slot (q+2)%3, own
@@ -780,13 +787,21 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
     C* const side = base + ((q + 2) % 3) * op.bufE;  // idle slot when the op stores nothing
     if (leader && nit < op.nitems) {
       if (Op::kStores) tma::bulk_wait_read<1>();  // slot nslot held the stores of step q-2
+#ifdef LSB_EXP_NOTMA
+      tma::mbar_expect_tx(&bar[nslot], 0);
+#else
       tma::mbar_expect_tx(&bar[nslot], op.load_bytes());
       op.load(nit, nst, base + nslot * op.bufE, &bar[nslot]);
+#endif
     }
     if constexpr (Op::kSideLoad) {
       if (leader && side_pending) {
+#ifdef LSB_EXP_NOTMA
+        tma::mbar_expect_tx(&bar[3 + (q & 1)], 0);
+#else
         tma::mbar_expect_tx(&bar[3 + (q & 1)], op.load_bytes());
         op.side_load(it, st, side, &bar[3 + (q & 1)]);
+#endif
       }
     }
     tma::mbar_wait(&bar[slot], (q / 3) & 1);
@@ -803,7 +818,9 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
       tma::fence_async_smem();
       __syncthreads();
       if (leader) {
+#ifndef LSB_EXP_NOTMA
         op.store(it, st, cur);
+#endif
         tma::bulk_commit();
       }
     } else {
@@ -959,7 +976,7 @@ template <typename R> struct TF1Op : OpBase {
     eng::dispatch<C>(sh.gcol(), true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       if constexpr (LGN > 0)
-        eng::for_first_slots<LGN, true, C>(typename F1Op<R>::template LoadM<LGN>{S, mhat, sh.ct(), t << sh.lgS});
+        eng::for_first_slots<LGN, true, C>(typename F1Op<R>::template LoadM<LGN>{S, mhat, sh.ct(), t << sh.lgS, scale});
     });
   }
   template <int LGN> struct F {
@@ -967,7 +984,7 @@ template <typename R> struct TF1Op : OpBase {
     const State& S;
     R scale;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
-      return cmul(S.mh[slot], b[nat_col<LGN, ST, C>(seq, j, r, 0)]) * scale;
+      return cmul(S.mh[slot], b[nat_col<LGN, ST, C>(seq, j, r, 0)]);
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, true>(seq, j, r)] = v; }
   };
@@ -1160,8 +1177,12 @@ template <typename R> struct TA2Op : A2Op<R> {
     bool issue;
     LS_D void pre_store() const {
       if (issue && threadIdx.x == 0) {
+#ifdef LSB_EXP_NOTMA
+        tma::mbar_expect_tx(nbar, 0);
+#else
         tma::mbar_expect_tx(nbar, op->load_bytes());
         op->side_load(it, knext, const_cast<C*>(b), nbar);
+#endif
       }
       tma::mbar_wait(bar, parity);
     }
