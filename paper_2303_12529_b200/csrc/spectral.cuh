@@ -41,6 +41,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 namespace lsb {
 namespace spec {
@@ -353,6 +354,7 @@ template <typename R> struct F1Op : OpBase {
   int lgnt;
   LS_D int steps(int it) const { return a.nk[it >> lgnt]; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
+  LS_D const C* field(int it, int k) const { return a.spec[it >> lgnt] + (size_t)k * fsz(); }  // column-tiled input
   LS_D void prefetch(int it, int k, C* b, C*) const {
     const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
     eng::gather_rect<sizeof(C)>(b, a.spec[set] + (size_t)k * fsz(), sh.ct(), 0, sh.lgH, t << sh.lgS, sh.lgS);
@@ -530,6 +532,7 @@ template <typename R> struct A2Op : OpBase {
   int lgnt;
   LS_D int steps(int it) const { return a.nk[it >> lgnt]; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
+  LS_D const C* field(int it, int k) const { return a.T[it >> lgnt] + (size_t)k * fsz(); }  // column-tiled U_k
   LS_D void prefetch(int it, int k, C* b, C*) const {
     const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
     eng::gather_rect<sizeof(C)>(b, a.T[set] + (size_t)k * fsz(), sh.ct(), 0, sh.lgH, t << sh.lgS, sh.lgS);
@@ -833,6 +836,159 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
   }
   if (leader && Op::kStores) tma::bulk_wait<0>();
   op.finish(S, reinterpret_cast<double*>(smraw));
+}
+
+// F1 on tall grids (k_pass_cluster): the transformed column stays in shared
+// memory; the cluster gathers each CTA's row quarter of the 4 columns back
+// through distributed shared memory and TMA stores it into the T_k tiles.
+template <typename R> struct F1COp : F1Op<R> {
+  using C = typename CT<R>::C;
+  using State = typename F1Op<R>::State;
+  static constexpr bool kGatherOut = true;
+  alignas(64) CUtensorMap tmap_T;  // T fields, 4-column x 256-row boxes
+  int koff[2];
+  template <int LGN> struct FS {
+    C* b;
+    const State& S;
+    template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
+      return cmul(S.mh[slot], b[nat_col<LGN, ST, C>(seq, j, r, 0)]);
+    }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_col<LGN, ST, C>(seq, j, r, 0)] = v; }
+  };
+  LS_D void step_smem(State& S, C* b) const {
+    const Geo g = this->sh.gcol();
+    eng::dispatch<C>(g, true, [&](auto fx) {
+      constexpr int LGN = decltype(fx)::LGN;
+      if constexpr (LGN > 0) {
+        FS<LGN> f{b, S};
+        eng::run_fix<LGN, true, true>(g, b, this->tw, f);
+      }
+    });
+  }
+  // rows [row0, row0 + rows) of the tile's 4 columns (natural [row][4]) -> T_k
+  LS_D void store_quarter(int itl, int k, int x0, int row0, int rows, const C* src) const {
+    const int set = itl >> this->lgnt;
+    constexpr int w = 1 << kLgTileT;
+    for (int b = 0; b * 256 < rows; ++b)
+      tma::tensor_s2g(&tmap_T, x0 & (w - 1), x0 >> kLgTileT, row0 + b * 256, k + koff[set], src + (size_t)b * 256 * 4);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Column passes on tall grids (8192-point columns, configs[4]): a column
+// item is one complex64 column, an 8-byte-wide slab of the 4-wide tiles, too
+// narrow for TMA; per-element cp.async / stores make the pass LSU-bound.
+// Here the four CTAs of a cluster take the four columns of one tile: each
+// CTA fetches a 64 KB row quarter of the tile (all four columns) with one
+// 1-D bulk copy, then the cluster scatters the quarters column-wise through
+// distributed shared memory, so each CTA holds its whole column; the
+// transform itself is the single-column op (F1Op / A2Op) unchanged.
+// Shared memory: the op's exchange buffer (the column) and two quarter
+// buffers, the next step's quarter streaming in while this step transforms.
+constexpr int kClusterCols = 4;
+template <class Op, class = void> struct has_gather_out : std::false_type {};
+template <class Op> struct has_gather_out<Op, std::void_t<decltype(Op::kGatherOut)>> : std::true_type {};
+
+template <typename R, class Op>
+__global__ void __cluster_dims__(kClusterCols, 1, 1) __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1)
+k_pass_cluster(const __grid_constant__ Op op, StopFlag stop, int ntiles, int nsets) {
+  using C = typename CT<R>::C;
+  using Vec = typename std::conditional<sizeof(C) == 8, float2, double2>::type;
+  if (stop && *stop) return;  // uniform across the cluster
+  extern __shared__ __align__(128) unsigned char smraw[];
+  C* const col = reinterpret_cast<C*>(smraw);
+  const size_t colE = (size_t)op.bufE;                       // elements (rounded to 128 B)
+  C* const quart = col + colE;                               // 2 x [H/4][4]
+  const int qrows = op.sh.H / kClusterCols, qE = qrows * kClusterCols;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(quart + 2 * (size_t)qE);
+  const unsigned rank = tma::cluster_rank();
+  const int cid = blockIdx.x / kClusterCols, ncl = gridDim.x / kClusterCols;
+  const int nit = ntiles * nsets;
+  const bool leader = threadIdx.x == 0;
+  if (leader) {
+    tma::mbar_init(&bar[0], 1);
+    tma::mbar_init(&bar[1], 1);
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  // the single-column op's item for (tile item, rank): column 4 t + rank of the set
+  auto legacy = [&](int it4) {
+    const int set = it4 / ntiles, t = it4 - set * ntiles;
+    return (set << op.lgnt) | (kClusterCols * t + (int)rank);
+  };
+  auto issue = [&](int it4, int k, int slot) {
+    const int t = it4 % ntiles;
+    const C* src = op.field(legacy(it4), k) + ((size_t)t * op.sh.H + (size_t)rank * qrows) * kClusterCols;
+    tma::mbar_expect_tx(&bar[slot], (unsigned)(qE * sizeof(C)));
+    tma::bulk_g2s(quart + (size_t)slot * qE, src, (unsigned)(qE * sizeof(C)), &bar[slot]);
+  };
+  if (cid >= nit) return;  // whole clusters idle together
+  typename Op::State S{};
+  int it4 = cid, st = 0;
+  if (leader) issue(it4, 0, 0);
+  for (unsigned q = 0;; ++q) {
+    const int slot = q & 1;
+    int nit4 = it4, nst = st + 1;  // next step
+    if (nst == op.steps(legacy(it4))) {
+      nst = 0;
+      nit4 += ncl;
+    }
+    tma::mbar_wait(&bar[slot], (q >> 1) & 1);
+    // every CTA's quarter has landed and every CTA is done with its column
+    tma::cluster_sync();
+    {
+      const C* qb = quart + (size_t)slot * qE;
+      unsigned dst[kClusterCols];
+#pragma unroll
+      for (int c = 0; c < kClusterCols; ++c) dst[c] = tma::cluster_map(col, c);
+      for (int i = threadIdx.x; i < qrows; i += blockDim.x) {
+        const Vec* row = reinterpret_cast<const Vec*>(qb + (size_t)i * kClusterCols);
+        const unsigned off = (unsigned)(((size_t)rank * qrows + i) * sizeof(C));
+#pragma unroll
+        for (int c = 0; c < kClusterCols; ++c) tma::st_cluster(dst[c] + off, row[c]);
+      }
+    }
+    tma::cluster_sync();  // columns complete; this step's quarters are free
+    if (leader && nit4 < nit) {
+      if constexpr (has_gather_out<Op>::value) tma::bulk_wait_read<0>();  // slot ^ 1 held step q-1's output
+      issue(nit4, nst, slot ^ 1);
+    }
+    const int itl = legacy(it4);
+    if (st == 0) op.begin(S, itl, col);
+    if constexpr (has_gather_out<Op>::value) {
+      op.step_smem(S, col);
+      tma::cluster_sync();  // every column transformed
+      // gather this CTA's row quarter of the 4 columns into the free quarter slot
+      C* ob = quart + (size_t)slot * qE;
+      unsigned srcs[kClusterCols];
+#pragma unroll
+      for (int c = 0; c < kClusterCols; ++c) srcs[c] = tma::cluster_map(col, c);
+      for (int i = threadIdx.x; i < qrows; i += blockDim.x) {
+        const unsigned off = (unsigned)(((size_t)rank * qrows + i) * sizeof(C));
+        Vec v[kClusterCols];
+#pragma unroll
+        for (int c = 0; c < kClusterCols; ++c) tma::ld_cluster(srcs[c] + off, v[c]);
+#pragma unroll
+        for (int c = 0; c < kClusterCols; ++c) reinterpret_cast<Vec*>(ob + (size_t)i * kClusterCols)[c] = v[c];
+      }
+      tma::fence_async_smem();
+      __syncthreads();
+      if (leader) {
+        const int t = it4 % ntiles;
+        op.store_quarter(itl, st, kClusterCols * t, (int)rank * qrows, qrows, ob);
+        tma::bulk_commit();
+      }
+    } else {
+      op.step(S, itl, st, col, nullptr);
+    }
+    if (st == op.steps(itl) - 1) op.end(S, itl, col, col);
+    it4 = nit4;
+    st = nst;
+    if (it4 >= nit) break;
+  }
+  if (leader && has_gather_out<Op>::value) tma::bulk_wait<0>();
+  // no CTA may exit while a sibling could still write into its shared memory
+  tma::cluster_sync();
 }
 
 // natural (dense) output position in a buffer; the TMA store box order
@@ -1263,6 +1419,55 @@ int launch_tma(Op& op, int threads, StopFlag stop, cudaStream_t s) {
   return grid;
 }
 
+// tall-grid column passes by 4-CTA clusters (k_pass_cluster): one complex64
+// column per CTA of a 4-wide tile layout
+template <typename R> bool cluster_ok(const Shape<R>& sh) {
+  using C = typename CT<R>::C;
+  static const bool off = [] {
+    const char* e = std::getenv("LSOPC_B200_NO_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  return !off && !tma_disabled() && sizeof(C) == 8 && sh.fast() && sh.lgS == 0 && sh.lgT == 2 &&
+         sh.W % kClusterCols == 0 && sh.H % (kClusterCols * 16) == 0;
+}
+template <typename R, class Op>
+void launch_cluster(Op& op, int ntiles, int nsets, StopFlag stop, cudaStream_t s) {
+  using C = typename CT<R>::C;
+  const size_t qE = (size_t)op.sh.H;  // a row quarter of a 4-wide tile: H/4 rows x 4
+  const size_t smem = (size_t)op.bufE * sizeof(C) + 2 * qE * sizeof(C) + 2 * sizeof(uint64_t);
+  if (smem > 227 * 1024) throw std::runtime_error("cluster column pass needs more than 227 KB of shared memory");
+  auto kern = k_pass_cluster<R, Op>;
+  // clusters live inside one GPC, so fewer than SMs / 4 may be co-resident:
+  // launch exactly as many as fit (the kernel loops over the items)
+  static int fit = 0;
+  static size_t fit_smem = 0;
+  if (!fit || fit_smem != smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sms() / kClusterCols * kClusterCols);
+    cfg.blockDim = dim3(eng::cta_threads<C>());
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = kClusterCols;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = num_sms() / kClusterCols;
+    }
+    fit = n;
+    fit_smem = smem;
+  }
+  const int nit = ntiles * nsets;
+  const int clusters = std::max(1, std::min(nit, fit));
+  kern<<<clusters * kClusterCols, eng::cta_threads<C>(), smem, s>>>(op, stop, ntiles, nsets);
+}
+
 // slot size for the TMA ring: the padded exchange buffer, rounded to 128 B
 template <typename R> int tma_bufE(int e) {
   using C = typename CT<R>::C;
@@ -1414,6 +1619,17 @@ void f1_impl(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, St
   f1.lgnt = g.lgW - sh.lgS;
   f1.bufE = col_bufE(sh);
   f1.nitems = (1 << f1.lgnt) * nsets;
+  if (cluster_ok(sh)) {
+    F1COp<R> fc;
+    static_cast<F1Op<R>&>(fc) = f1;
+    fc.bufE = tma_bufE<R>(col_bufE(sh));
+    const int ew = sizeof(C) / 8;
+    fc.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), (unsigned)(kClusterCols * ew),
+                               1, 256);
+    for (int i = 0; i < 2; ++i) fc.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+    launch_cluster<R>(fc, g.W / kClusterCols, nsets, stop, s);
+    return;
+  }
   launch_op<R>(f1, col_threads(sh), 0, stop, s);
 }
 
@@ -1513,6 +1729,11 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
   a2.lgnt = g.lgW - sh.lgS;
   a2.bufE = col_bufE(sh);
   a2.nitems = (1 << a2.lgnt) * nsets;
+  if (cluster_ok(sh)) {
+    a2.bufE = tma_bufE<R>(col_bufE(sh));
+    launch_cluster<R>(a2, g.W / kClusterCols, nsets, stop, s);
+    return;
+  }
   launch_op<R>(a2, col_threads(sh), 0, stop, s);
 }
 

@@ -146,3 +146,21 @@ def test_strips_match_single_tile(world):
         assert np.allclose(h, hr, rtol=1e-9, atol=1e-12)
         assert np.array_equal(mask, mr)
         assert (l2r, pvbr) == (l2, pvb)
+
+
+@pytest.mark.gpu
+def test_tall_grid_cluster_column_passes_match_single_column_path():
+    """8192-point columns (configs[4] windows) run F1 / A2 on 4-CTA clusters
+    (distributed-shared-memory column scatter, k_pass_cluster); the same
+    solve with the clusters disabled takes the single-column passes.  Inputs
+    bit-identical, outputs within float32 rounding."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    script = Path(__file__).resolve().parents[1] / "scripts" / "cluster_check.py"
+    p = subprocess.run([sys.executable, str(script), "8192", "256"], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout + p.stderr
+    line = p.stdout.strip().splitlines()[-1]
+    rel = float(line.split("rel diff ")[1].split(",")[0])
+    assert rel <= 1e-6, line
+    assert line.endswith("final mask xor 0"), line
