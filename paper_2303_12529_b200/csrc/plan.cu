@@ -112,7 +112,7 @@ void check_kset(const lsopc_plan* p, const lsopc_kset* k) {
 
 double reduce_to_host(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
                       lsopc_plan* plan, cudaStream_t s, int W = 0, int ix0 = 0, int ix1 = 0) {
-  DevBuf tmp;
+  thread_local DevBuf tmp;  // plan-less calls: per-thread partials, kept across calls
   double* part;
   double* out;
   if (plan) {
@@ -128,7 +128,6 @@ double reduce_to_host(int op, size_t n, const double* a, const double* b, const 
   double h = 0.0;
   ck(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, s), "memcpy");
   ck(cudaStreamSynchronize(s), "sync");
-  tmp.release();
   return h;
 }
 
@@ -381,7 +380,9 @@ int lsopc_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_lower
     const size_t n = (size_t)H * W;
     double diff = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, mask, nullptr, nullptr, s);
     if (diff == 0.0 || diff == (double)n) throw Error(LSOPC_EDEGENERATE, "mask is uniform: no boundary exists");
-    DevBuf si, sf;
+    // scratch kept per calling thread: a cudaMalloc / cudaFree pair per call
+    // (cudaFree synchronises the device) cost more than the transform
+    thread_local DevBuf si, sf;
     si.ensure(tsdf_scratch_i32(H, W) * sizeof(int));
     sf.ensure(tsdf_scratch_f64(H, W) * sizeof(double));
     launch_tsdf(H, W, mask, d_upper, d_lower, phi, si.as<int>(), sf.as<double>(), s);
