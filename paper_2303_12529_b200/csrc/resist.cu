@@ -23,18 +23,6 @@ constexpr int kRedThreads = 256;
 
 LS_D double sigmoid(double i, double i_th, double sz) { return 1.0 / (1.0 + exp(-sz * (i - i_th))); }
 
-// fp32 tier: Z and the gate Z (1 - Z) (Z - Z_t) in float from the float
-// intensity, 1 - Z formed as e / (1 + e) (no cancellation near Z = 1); the
-// loss sums accumulate in double
-struct ZF {
-  float z, omz;  // Z, 1 - Z
-};
-LS_D ZF sigmoid_f(float i, float i_th, float sz) {
-  const float e = expf(-sz * (i - i_th));
-  const float r = 1.0f / (1.0f + e);
-  return ZF{r, e * r};
-}
-
 template <typename R>
 __global__ void __launch_bounds__(kRedThreads)
 k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uint8_t* __restrict__ tu8,
@@ -59,26 +47,6 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
       if (h_in) h_in[i] = i_in >= p.i_th;
     }
     if (!z_nom && !wf && !partials) continue;
-    if constexpr (sizeof(R) == 4) {
-      if (!z_nom && have_t) {  // the DSO loop's form: losses + gates only
-        const float fth = (float)p.i_th, fsz = (float)p.sigma_z;
-        const ZF n = sigmoid_f((float)i_nom, fth, fsz), o = sigmoid_f((float)i_out, fth, fsz),
-                 d = sigmoid_f((float)i_in, fth, fsz);
-        const float zt = tu8 ? (float)tu8[i] : (float)tf[i];
-        const float dn = n.z - zt, di = d.z - zt, dout = o.z - zt;
-        const int x = whole ? ix0 : (int)col_of(rs, i);
-        if (x >= ix0 && x < ix1) {
-          acc[0] += (double)dn * dn;
-          acc[1] += (double)di * di + (double)dout * dout;
-        }
-        if (wf) {
-          const float gn = dn * n.z * n.omz, go = dout * o.z * o.omz, gi = di * d.z * d.omz;
-          wf[i] = (R)(p.alpha * gn + p.beta * 1.02 * go);
-          wd[i] = (R)(p.beta * 0.98 * gi);
-        }
-        continue;
-      }
-    }
     double zn = sigmoid(i_nom, p.i_th, p.sigma_z);
     double zo = sigmoid(i_out, p.i_th, p.sigma_z);
     double zi = sigmoid(i_in, p.i_th, p.sigma_z);
@@ -147,59 +115,35 @@ k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, con
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n4; g += (size_t)gridDim.x * blockDim.x) {
     const size_t i = 4 * g;
     R sf[4], sd[4] = {(R)0, (R)0, (R)0, (R)0};
-    R zt[4];
+    double zt[4];
     ld4(If, i, sf);
     if (Id) ld4(Id, i, sd);
     if (tu8) {  // binary targets: a select, not an int->float conversion
       const uchar4 t = *reinterpret_cast<const uchar4*>(tu8 + i);
       const unsigned char tv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) zt[e] = tv[e] == 0 ? (R)0 : tv[e] == 1 ? (R)1 : (R)tv[e];
+      for (int e = 0; e < 4; ++e) zt[e] = (double)tv[e];
     } else {
-      double t[4];
-      ld4(tf, i, t);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) zt[e] = (R)t[e];
+      ld4(tf, i, zt);
     }
     const int x0 = whole ? ix0 : (int)col_of(rs, i);
     R gf[4], gd[4];
-    if constexpr (sizeof(R) == 4) {
-      // all-float arithmetic (conversions run on the narrow XU pipe); each
-      // 4-pixel group's loss terms are summed in float, then in double
-      const float fth = (float)p.i_th, fsz = (float)p.sigma_z, fa = (float)p.alpha, fbo = (float)(p.beta * 1.02),
-                  fbi = (float)(p.beta * 0.98);
-      float s0 = 0.f, s1 = 0.f;
+    // float64 sigmoid and gates in both tiers: the loop's losses agree with the
+    // API path (print_corners / ilt_loss) on the same intensities
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const ZF zn = sigmoid_f(fmaxf(sf[e], 0.f), fth, fsz), zo = sigmoid_f(fmaxf(1.02f * sf[e], 0.f), fth, fsz),
-                 zi = sigmoid_f(Id ? fmaxf(0.98f * sd[e], 0.f) : 0.f, fth, fsz);
-        const float t = (float)zt[e];
-        const float dn = zn.z - t, di = zi.z - t, dout = zo.z - t;
-        if (whole || (x0 + e >= ix0 && x0 + e < ix1)) {
-          s0 += dn * dn;
-          s1 += di * di + dout * dout;
-        }
-        gf[e] = fa * (dn * zn.z * zn.omz) + fbo * (dout * zo.z * zo.omz);
-        gd[e] = fbi * (di * zi.z * zi.omz);
+    for (int e = 0; e < 4; ++e) {
+      const double i_nom = fmax(1.0 * (double)sf[e], 0.0);
+      const double i_out = fmax(1.02 * (double)sf[e], 0.0);
+      const double i_in = Id ? fmax(0.98 * (double)sd[e], 0.0) : 0.0;
+      const double zn = sigmoid(i_nom, p.i_th, p.sigma_z), zo = sigmoid(i_out, p.i_th, p.sigma_z),
+                   zi = sigmoid(i_in, p.i_th, p.sigma_z);
+      const double dn = zn - zt[e], di = zi - zt[e], dout = zo - zt[e];
+      if (whole || (x0 + e >= ix0 && x0 + e < ix1)) {
+        acc[0] += dn * dn;
+        acc[1] += di * di + dout * dout;
       }
-      acc[0] += (double)s0;
-      acc[1] += (double)s1;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const double i_nom = fmax(1.0 * (double)sf[e], 0.0);
-        const double i_out = fmax(1.02 * (double)sf[e], 0.0);
-        const double i_in = Id ? fmax(0.98 * (double)sd[e], 0.0) : 0.0;
-        const double zn = sigmoid(i_nom, p.i_th, p.sigma_z), zo = sigmoid(i_out, p.i_th, p.sigma_z),
-                     zi = sigmoid(i_in, p.i_th, p.sigma_z);
-        const double dn = zn - zt[e], di = zi - zt[e], dout = zo - zt[e];
-        if (whole || (x0 + e >= ix0 && x0 + e < ix1)) {
-          acc[0] += dn * dn;
-          acc[1] += di * di + dout * dout;
-        }
-        gf[e] = (R)(p.alpha * (dn * zn * (1.0 - zn)) + p.beta * 1.02 * (dout * zo * (1.0 - zo)));
-        gd[e] = (R)(p.beta * 0.98 * (di * zi * (1.0 - zi)));
-      }
+      gf[e] = (R)(p.alpha * (dn * zn * (1.0 - zn)) + p.beta * 1.02 * (dout * zo * (1.0 - zo)));
+      gd[e] = (R)(p.beta * 0.98 * (di * zi * (1.0 - zi)));
     }
     if (wf) {
       st4(wf, i, gf);
