@@ -116,7 +116,7 @@ template <int RAD, typename C> LS_D void dft(C* v) {
 
 // ---- buffer geometry ---------------------------------------------------------
 
-template <typename C> constexpr int pad_shift() { return sizeof(C) == 8 ? 4 : 3; }
+template <typename C> constexpr int pad_shift() { return 4; }  // 1 pad element per 16: 16j+r -> 17j+r, conflict-free first-stage writes for 8- and 16-byte elements
 template <typename C> LS_HD int padded(int i) { return i + (i >> pad_shift<C>()); }
 template <typename C> LS_HD int padded_len(int n) { return n + (n >> pad_shift<C>()) + 1; }
 // elements of one stage buffer holding S sequences of length n (natural or padded)
