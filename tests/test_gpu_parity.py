@@ -243,6 +243,17 @@ def test_tsdf_clip_2048():
     assert np.array_equal(b2.tsdf_from_mask(clip).phi, o.tsdf(clip))
 
 
+def test_tsdf_truncation_shortcut_is_exact():
+    """The row scan stops at the truncation distance: far pixels (d > D_u + 1)
+    and deep pixels (d > 1 - D_l) must still match the exact EDT bit for bit,
+    for the default bounds and for bounds far larger / smaller than the grid."""
+    m = np.zeros((1100, 1100), dtype=np.uint8)
+    m[17, 1050] = 1                  # one lit pixel: distances up to ~1500 px
+    m[600:1000, 100:700] = 1         # and a large block: interior distances up to 200
+    for up, lo in ((900.0, -100.0), (1e7, -1e7), (3.0, -2.0)):
+        assert np.array_equal(b2.tsdf_from_mask(m, up, lo).phi, o.tsdf(m, up, lo)), (up, lo)
+
+
 def test_tsdf_uniform_rejected():
     with pytest.raises(b2.DegenerateInputError):
         b2.tsdf_from_mask(np.zeros((8, 8), dtype=np.uint8))

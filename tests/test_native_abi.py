@@ -145,3 +145,21 @@ def test_fracture_matches_reference_rect_lists():
     for i in range(12):
         got = metrics.fracture(g[f"mask{i}"])
         assert got == [tuple(int(v) for v in r) for r in g[f"rects{i}"]]
+
+
+def test_fracture_on_lit_bounding_box_is_translation_exact():
+    """The native fracture works on the bounding box of the lit pixels; a
+    reference rectangle list embedded at an offset in an empty frame must come
+    back unchanged up to that offset (the (area, top, left) order is
+    translation invariant), including masks touching the frame's edges."""
+    from paper_2303_12529_b200 import metrics
+    g = golden("fracture")
+    for i in range(12):
+        m = g[f"mask{i}"]
+        ref = [tuple(int(v) for v in r) for r in g[f"rects{i}"]]
+        for oy, ox, H, W in ((5, 9, 80, 96), (0, 0, m.shape[0] + 3, m.shape[1] + 7),
+                             (7, 0, m.shape[0] + 7, m.shape[1])):
+            big = np.zeros((H, W), dtype=np.uint8)
+            big[oy:oy + m.shape[0], ox:ox + m.shape[1]] = m
+            got = metrics.fracture(big)
+            assert got == [(x + ox, y + oy, w, h) for x, y, w, h in ref], (i, oy, ox)
