@@ -56,6 +56,9 @@ constexpr int kMaxK = 64;  // kernels per set carried in a launch
 // tiling at full speed, while a 4-column item of an 8-wide tiling runs at 91%).
 // U_k, V, M^, spectra: 32 B tile rows, so a column item (4 x c64 or 2 x c128) is a whole tile
 template <typename C> constexpr int lg_tile() { return sizeof(C) == 8 ? 2 : 1; }
+// tall grids split four ways (k_f1_split): natural row y of T_k / U_k / V is
+// stored at row (y mod 4) * H/4 + y / 4
+LS_HD int split_row(int y, int lgq) { return ((y & 3) << lgq) | (y >> 2); }
 constexpr int kLgTileT = 3;  // T_k: read by the F2 row pass as 256 B chunks
 
 template <typename R> struct Shape {
@@ -1167,6 +1170,7 @@ template <typename R> struct TF2Op : OpBase {
   SetArgs<R> a;
   const C* tw;
   int lgnb;
+  int split_lgq;                   // >= 0: T rows stored in split order (split_row)
   alignas(64) CUtensorMap tmap_T;  // T fields, row-item boxes
   int koff[2];
   LS_D int steps(int it) const { return a.nk[it >> lgnb]; }
@@ -1175,9 +1179,11 @@ template <typename R> struct TF2Op : OpBase {
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
     const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     const int tiles = sh.W >> kLgTileT, bt = tiles < 256 ? tiles : 256;
-    for (int r = 0; r < (1 << sh.lgR); ++r)
+    for (int r = 0; r < (1 << sh.lgR); ++r) {
+      const int yr = split_lgq >= 0 ? split_row(y0 + r, split_lgq) : y0 + r;
       for (int b = 0; b * bt < tiles; ++b)
-        tma::tensor_g2s(dst + (r << sh.lgW) + ((b * bt) << kLgTileT), &tmap_T, 0, b * bt, y0 + r, k + koff[set], bar);
+        tma::tensor_g2s(dst + (r << sh.lgW) + ((b * bt) << kLgTileT), &tmap_T, 0, b * bt, yr, k + koff[set], bar);
+    }
   }
   LS_D void store(int it, int k, const C* src) const {
     const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
@@ -1419,6 +1425,172 @@ int launch_tma(Op& op, int threads, StopFlag stop, cudaStream_t s) {
   return grid;
 }
 
+// ---------------------------------------------------------------------------
+// Tall grids, four-step split (H = 4M, M = 2048, complex64): the column
+// transform of a 4-column tile is split across the 4-CTA cluster so every
+// CTA runs the fast 4-column 2048-point engine.  With f = f2 + M c and
+// n = 4 m + k1 (N = 4M):
+//   inverse  x[4m + k1] = IFFT_M( y_k1 )[m],
+//            y_k1[f2] = e^{+2 pi i f2 k1 / N} sum_c P[f2 + M c] i^{c k1}
+// so F1 does the radix-4 step first: CTA r fetches the rows it combines
+// (f2 in [M r / 4, M (r+1) / 4) at the four offsets M c: four 16 KB strips, one
+// bulk copy each), forms y_k1 and pushes it to CTA k1 through distributed
+// shared memory; then each CTA runs the local 4-column 2048-point inverse.
+// CTA k1's output rows 4 m + k1 are stored as T_k rows k1 M + m (the row
+// permutation `split_row`, undone by F2's per-row loads).  Measured (8192 x
+// 2048 window): F1 8.3 -> 7.0 ms; the two cluster barriers per step
+// (MEMBAR / ERRBAR / UCGABAR stalls in ncu) and the 64 KB of DSMEM stores per
+// CTA per step are now the cost.  The adjoint column pass (A2) keeps the
+// single-column cluster path.
+constexpr int kSplitM = 2048;
+LS_D float2 mul_ipow(float2 z, int e) {  // z * i^e
+  switch (e & 3) {
+    case 0: return z;
+    case 1: return make_float2(-z.y, z.x);
+    case 2: return make_float2(-z.x, -z.y);
+    default: return make_float2(z.y, -z.x);
+  }
+}
+LS_D void ld_row4(unsigned addr, float2 (&v)[4]) {
+  const float4 a = tma::ld_cluster_f4(addr), b = tma::ld_cluster_f4(addr + 16);
+  v[0] = make_float2(a.x, a.y);
+  v[1] = make_float2(a.z, a.w);
+  v[2] = make_float2(b.x, b.y);
+  v[3] = make_float2(b.z, b.w);
+}
+LS_D void st_row4(unsigned addr, const float2 (&v)[4]) {
+  tma::st_cluster_f4(addr, make_float4(v[0].x, v[0].y, v[1].x, v[1].y));
+  tma::st_cluster_f4(addr + 16, make_float4(v[2].x, v[2].y, v[3].x, v[3].y));
+}
+
+struct F1SplitArgs {
+  Shape<float> sh;
+  SetArgs<float> a;
+  const float2* mhat;
+  float scale;
+  const float2* tw;  // N entries, e^{-2 pi i j / N}
+  int ntiles, nsets, bufE, lgnmax;
+  alignas(64) CUtensorMap tmap_T;
+  int koff[2];
+};
+
+// in-place natural [row][4] transform of the local quarter
+template <int LGN> struct SplitF {
+  float2* b;
+  template <int ST> LS_D float2 load(int seq, int j, int r, int) const { return b[nat_col<LGN, ST, float2>(seq, j, r, 0)]; }
+  template <int ST> LS_D void store(int seq, int j, int r, float2 v, int) { b[nat_col<LGN, ST, float2>(seq, j, r, 0)] = v; }
+};
+
+template <int V = 0>  // a template: the header is compiled in several translation units
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
+k_f1_split(const __grid_constant__ F1SplitArgs A, StopFlag stop) {
+  using C = float2;
+  constexpr int M = kSplitM, QE = M * 4, Q4 = M / 4;
+  if (stop && *stop) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  C* const work = reinterpret_cast<C*>(smraw);
+  C* const in = work + A.bufE;  // 2 x [M][4]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(in + 2 * QE);
+  const unsigned rank = tma::cluster_rank();
+  const int cid = blockIdx.x / 4, ncl = gridDim.x / 4, nit = A.ntiles * A.nsets;
+  const bool leader = threadIdx.x == 0;
+  const int H = A.sh.H, lgq = 11;  // storage quarter = 2^11 rows
+  if (leader) {
+    tma::mbar_init(&bar[0], 1);
+    tma::mbar_init(&bar[1], 1);
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  if (cid >= nit) return;
+  // this CTA's rows of the radix-4 step: f2 in [Q4 r, Q4 (r+1)) at the four
+  // offsets M c -- four contiguous 16 KB strips of the tile, one bulk copy each
+  auto issue = [&](int it4, int k, int slot) {
+    const int set = it4 / A.ntiles, t = it4 - set * A.ntiles;
+    const C* tile = A.a.spec[set] + (size_t)k * H * A.sh.W + (size_t)t * H * 4;
+    tma::mbar_expect_tx(&bar[slot], (unsigned)(QE * sizeof(C)));
+    for (int c = 0; c < 4; ++c)
+      tma::bulk_g2s(in + (size_t)slot * QE + (size_t)c * Q4 * 4, tile + ((size_t)M * c + (size_t)Q4 * rank) * 4,
+                    (unsigned)(Q4 * 4 * sizeof(C)), &bar[slot]);
+  };
+  unsigned addr_work[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) addr_work[c] = tma::cluster_map(work, c);
+  const int f2 = Q4 * (int)rank + (int)threadIdx.x;  // this thread's row of the radix-4 step
+  C mh[4][4];                                        // M^ at rows f2 + M c, 4 columns
+  int it4 = cid, st = 0;
+  if (leader) issue(it4, 0, 0);
+  for (unsigned q = 0;; ++q) {
+    const int slot = q & 1, set = it4 / A.ntiles, t = it4 - set * A.ntiles, nk = A.a.nk[set];
+    int nit4 = it4, nst = st + 1;
+    if (nst == nk) {
+      nst = 0;
+      nit4 += ncl;
+    }
+    if (st == 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4* row = reinterpret_cast<const float4*>(A.mhat + ((size_t)t * H + f2 + (size_t)M * c) * 4);
+        const float4 u = __ldg(row), v = __ldg(row + 1);
+        mh[c][0] = make_float2(u.x * A.scale, u.y * A.scale);
+        mh[c][1] = make_float2(u.z * A.scale, u.w * A.scale);
+        mh[c][2] = make_float2(v.x * A.scale, v.y * A.scale);
+        mh[c][3] = make_float2(v.z * A.scale, v.w * A.scale);
+      }
+    }
+    if (leader && nit4 < nit) issue(nit4, nst, slot ^ 1);  // the other strip buffer was consumed last step
+    tma::mbar_wait(&bar[slot], (q >> 1) & 1);
+    if (leader) tma::bulk_wait_read<0>();  // the previous step's T store has read `work`
+    tma::cluster_sync();                     // every CTA's `work` is free
+    {
+      C p[4][4];
+      const C* strips = in + (size_t)slot * QE;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4* row = reinterpret_cast<const float4*>(strips + ((size_t)c * Q4 + threadIdx.x) * 4);
+        const float4 u = row[0], v = row[1];
+        const C h[4] = {make_float2(u.x, u.y), make_float2(u.z, u.w), make_float2(v.x, v.y), make_float2(v.z, v.w)};
+#pragma unroll
+        for (int col = 0; col < 4; ++col) p[c][col] = cmul(mh[c][col], h[col]);
+      }
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) {
+        const C w = cconj(__ldg(&A.tw[f2 * k1]));
+        C y[4];
+#pragma unroll
+        for (int col = 0; col < 4; ++col) {
+          C acc = p[0][col];
+#pragma unroll
+          for (int c = 1; c < 4; ++c) acc = acc + mul_ipow(p[c][col], c * k1);
+          y[col] = k1 ? cmul(acc, w) : acc;
+        }
+        st_row4(addr_work[k1] + (unsigned)(f2 * 4 * sizeof(C)), y);
+      }
+    }
+    // (st.async with per-row mbarrier completion in place of this barrier measured slower)
+    tma::cluster_sync();  // every CTA's y quarter complete
+    {
+      const Geo g{11, 2, A.lgnmax - 11};
+      SplitF<11> f{work};
+      eng::run_fix<11, true, true>(g, work, A.tw, f);
+    }
+    tma::fence_async_smem();
+    __syncthreads();
+    if (leader) {
+      constexpr int w = 1 << kLgTileT;
+      const int x0 = 4 * t;
+      for (int b = 0; b * 256 < M; ++b)
+        tma::tensor_s2g(&A.tmap_T, x0 & (w - 1), x0 >> kLgTileT, ((int)rank << lgq) + b * 256, st + A.koff[set],
+                        work + (size_t)b * 256 * 4);
+      tma::bulk_commit();
+    }
+    it4 = nit4;
+    st = nst;
+    if (it4 >= nit) break;
+  }
+  if (leader) tma::bulk_wait<0>();
+  tma::cluster_sync();
+}
+
 // tall-grid column passes by 4-CTA clusters (k_pass_cluster): one complex64
 // column per CTA of a 4-wide tile layout
 template <typename R> bool cluster_ok(const Shape<R>& sh) {
@@ -1430,6 +1602,45 @@ template <typename R> bool cluster_ok(const Shape<R>& sh) {
   return !off && !tma_disabled() && sizeof(C) == 8 && sh.fast() && sh.lgS == 0 && sh.lgT == 2 &&
          sh.W % kClusterCols == 0 && sh.H % (kClusterCols * 16) == 0;
 }
+// four-step split path (k_f1_split / k_a2_split): H = 4 * 2048 complex64 rows
+template <typename R> bool split_ok(const Shape<R>& sh) {
+  static const bool off = [] {
+    const char* e = std::getenv("LSOPC_B200_NO_SPLIT");
+    return e && e[0] == '1';
+  }();
+  return !off && cluster_ok(sh) && sh.H == 4 * kSplitM && sh.W <= sh.H;
+}
+inline int max_clusters(const void* kern, int threads, size_t smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms() / 4 * 4);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 4;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = num_sms() / 4;
+  }
+  return n;
+}
+inline void launch_f1_split(F1SplitArgs& A, StopFlag stop, cudaStream_t s) {
+  const size_t smem = (size_t)A.bufE * sizeof(float2) + 2 * (size_t)kSplitM * 4 * sizeof(float2) + 2 * sizeof(uint64_t);
+  static int fit = 0;
+  if (!fit) {
+    cudaFuncSetAttribute(k_f1_split<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_f1_split<0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    fit = max_clusters((const void*)k_f1_split<0>, 512, smem);
+  }
+  const int clusters = std::max(1, std::min(A.ntiles * A.nsets, fit));
+  k_f1_split<0><<<clusters * 4, 512, smem, s>>>(A, stop);
+}
+
 template <typename R, class Op>
 void launch_cluster(Op& op, int ntiles, int nsets, StopFlag stop, cudaStream_t s) {
   using C = typename CT<R>::C;
@@ -1619,6 +1830,25 @@ void f1_impl(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, St
   f1.lgnt = g.lgW - sh.lgS;
   f1.bufE = col_bufE(sh);
   f1.nitems = (1 << f1.lgnt) * nsets;
+  if constexpr (sizeof(C) == 8) {
+    if (split_ok(sh)) {
+      F1SplitArgs A;
+      A.sh = sh;
+      A.a = a;
+      A.mhat = static_cast<const float2*>(mhat);
+      A.scale = (float)(1.0 / (double)g.n());
+      A.tw = static_cast<const float2*>(g.tw);
+      A.ntiles = g.W / 4;
+      A.nsets = nsets;
+      A.lgnmax = g.lgnmax;
+      // the local buffer holds 4 columns x 2048 rows with the exchange padding
+      A.bufE = tma_bufE<R>(align_elems<R>(eng::buf_elems<C>(kSplitM, 4)));
+      A.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, 1}, g.H, g.W, total_nk(a), 4u, 1, 256);
+      for (int i = 0; i < 2; ++i) A.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+      launch_f1_split(A, stop, s);
+      return;
+    }
+  }
   if (cluster_ok(sh)) {
     F1COp<R> fc;
     static_cast<F1Op<R>&>(fc) = f1;
@@ -1644,6 +1874,7 @@ void f2_impl(const Grid& g, const SpecSet* sets, int nsets, double2* a0_out, Sto
     f2.a = a;
     f2.tw = static_cast<const C*>(g.tw);
     f2.lgnb = g.lgH - sh.lgR;
+    f2.split_lgq = split_ok(sh) ? 11 : -1;
     const int ew = sizeof(C) / 8, tiles = g.W >> kLgTileT;
     f2.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), (unsigned)((1 << kLgTileT) * ew),
                                (unsigned)std::min(tiles, 256), 1);
