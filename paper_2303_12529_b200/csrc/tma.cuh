@@ -122,13 +122,6 @@ __device__ __forceinline__ void st_cluster_f4(unsigned addr, float4 v) {
                "f"(v.w)
                : "memory");
 }
-// asynchronous remote store: completes `16` transaction bytes on the
-// destination CTA's mbarrier `mbar` (both shared::cluster addresses)
-__device__ __forceinline__ void st_async_f4(unsigned addr, float4 v, unsigned mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(addr),
-               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(mbar)
-               : "memory");
-}
 __device__ __forceinline__ void st_cluster(unsigned addr, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }

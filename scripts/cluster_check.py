@@ -19,7 +19,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "run":
 import numpy as np
 H, W = (int(a) for a in sys.argv[1:3]) if len(sys.argv) > 2 else (8192, 256)
 out = {}
-for tag, env in (("cluster", {}), ("single", {"LSOPC_B200_NO_CLUSTER": "1"})):
+extra = sys.argv[3] if len(sys.argv) > 3 else ""          # e.g. LSOPC_B200_NO_SPLIT=1
+env_extra = dict([extra.split("=")]) if extra else {}
+for tag, env in (("cluster", env_extra), ("single", {"LSOPC_B200_NO_CLUSTER": "1"})):
     p = subprocess.run([sys.executable, __file__, "run", str(H), str(W), f"/tmp/cc_{tag}.npy"], capture_output=True,
                        text=True, env={**os.environ, **env})
     if p.returncode:

@@ -158,9 +158,11 @@ def test_tall_grid_cluster_column_passes_match_single_column_path():
     import sys
     from pathlib import Path
     script = Path(__file__).resolve().parents[1] / "scripts" / "cluster_check.py"
-    p = subprocess.run([sys.executable, str(script), "8192", "256"], capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout + p.stderr
-    line = p.stdout.strip().splitlines()[-1]
-    rel = float(line.split("rel diff ")[1].split(",")[0])
-    assert rel <= 1e-6, line
-    assert line.endswith("final mask xor 0"), line
+    for extra in ([], ["LSOPC_B200_NO_SPLIT=1"]):  # four-step split F1, then the single-column cluster F1
+        p = subprocess.run([sys.executable, str(script), "8192", "256", *extra], capture_output=True, text=True,
+                           timeout=600)
+        assert p.returncode == 0, p.stdout + p.stderr
+        line = p.stdout.strip().splitlines()[-1]
+        rel = float(line.split("rel diff ")[1].split(",")[0])
+        assert rel <= 1e-6, (extra, line)
+        assert line.endswith("final mask xor 0"), (extra, line)
