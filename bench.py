@@ -65,10 +65,35 @@ def dist_env():
 
 
 def peaks():
+    """Roofline denominators: the driver's MEASURED_PEAKS.json (STREAM-style
+    copy `hbm_gbs`), else the profiling guide's fallback."""
     try:
-        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+        pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        if float(pk.get("hbm_gbs", 0)) > 0:
+            return pk, "measured"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+        pass
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def copy_rate_gbs(gib=2, reps=5):
+    """Device-to-device copy rate of this GPU right now (read + write bytes),
+    for context beside the roofline denominator."""
+    import torch
+    a = torch.empty(gib << 27, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    a.fill_(1.0)
+    b.copy_(a)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    del a, b
+    return 2.0 * (gib << 30) / (ms * 1e6)
 
 
 # ---------------------------------------------------------------------------
@@ -256,6 +281,7 @@ def b200_arm(args, world, rank, local):
     # ---- per-pass CUDA-event timing on the session stream (after the timed region)
     pk, src = peaks()
     hbm = float(pk["hbm_gbs"])
+    copy_gbs = copy_rate_gbs()
     ms_pass = (ctypes.c_double * 8)()
     nv.check(L.lsopc_session_time_passes(sess, 5, ms_pass))
     L.lsopc_session_destroy(sess)
@@ -411,6 +437,8 @@ def b200_arm(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": round(per_pass[dom]["gbs"], 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(per_pass[dom]["frac"], 4), "traffic": traffic,
                      "kernel": per_pass[dom]["name"], "peak_source": src,
+                     "copy_GBps_measured": round(copy_gbs, 1),
+                     "frac_of_copy": round(per_pass[dom]["gbs"] / copy_gbs, 4),
                      "per_pass": {per_pass[w]["name"]: {"us": round(per_pass[w]["us"], 2),
                                                         "GBps": round(per_pass[w]["gbs"], 1),
                                                         "frac": round(per_pass[w]["frac"], 4)}
