@@ -400,6 +400,34 @@ def test_clip2048_iteration0_fp32():
     assert abs(b2.pvband(hard.inner, hard.outer) - int(g["hard_pvb"])) <= 4
 
 
+def test_clip2048_iteration0_fp64():
+    """The exact tier at full size (2048^2, N_k = 24): the same quantities as
+    the fp32 test against the reference's own output, at float64 tolerances,
+    and the hard prints' L2 / PVB exactly."""
+    nv.set_precision("fp64")
+    g = golden("clip2048")
+    f, d, F, D = kernels(35, 24, 4)
+    clip = o.iccad_like_clip(0)
+    mask = clip.astype(np.float64)
+    cfg = b2.OptConfig()
+    p = b2.print_corners(mask, F, D, cfg, binarize=False)
+    ys, xs = g["ys"], g["xs"]
+    assert np.abs(p.nominal[ys, xs] - g["z_nom"]).max() <= 1e-10
+    assert np.abs(p.inner[ys, xs] - g["z_in"]).max() <= 1e-10
+    assert np.abs(p.outer[ys, xs] - g["z_out"]).max() <= 1e-10
+    l_ilt = b2.ilt_loss(p.nominal, clip)
+    l_pvb = b2.pvb_loss(p.inner, p.outer, clip)
+    assert abs(l_ilt - g["l_ilt"]) <= 1e-10 * g["l_ilt"]
+    assert abs(l_pvb - g["l_pvb"]) <= 1e-10 * g["l_pvb"]
+    gi = b2.ilt_gradient(mask, p.nominal, clip, F, cfg)
+    gp = b2.pvb_gradient(mask, p.inner, p.outer, clip, F, D, cfg)
+    v = b2.velocity(gi, gp, cfg)
+    assert np.abs(v[ys, xs] - g["v"]).max() <= 1e-9 * g["v_absmax"]
+    hard = b2.print_corners(mask, F, D, cfg, binarize=True)
+    assert b2.l2_error(hard.nominal, clip) == int(g["hard_l2"])
+    assert b2.pvband(hard.inner, hard.outer) == int(g["hard_pvb"])
+
+
 def test_modulation_search_small():
     nv.set_precision("fp64")
     f, d, F, D = kernels(9, 2, 2)
