@@ -213,8 +213,10 @@ def _forward_losses(mask, target, focus_kernels, defocus_kernels, cfg):
 
 
 def _check_target(target):
-    t = (np.asarray(target) != 0).astype(np.uint8)
-    if t.all() or not t.any():
+    # one comparison pass (bool viewed as 0/1 bytes) and one count
+    t = np.not_equal(np.asarray(target), 0).view(np.uint8)
+    nz = int(np.count_nonzero(t))
+    if nz == 0 or nz == t.size:
         raise DegenerateInputError("target layout is uniform")
     return t
 
