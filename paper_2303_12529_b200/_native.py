@@ -181,6 +181,32 @@ def pinned_like(t):
     return buf
 
 
+_h2d_done = {}
+
+
+def to_dev_staged(a, dtype=np.uint8):
+    """Host array -> new device tensor through a cached page-locked staging
+    buffer (per shape, dtype and lane); an event guards the buffer against
+    being overwritten while its previous upload is still in flight."""
+    t = torch()
+    arr = np.asarray(a, dtype=dtype)
+    key = ("h2d", arr.shape, arr.dtype.str, lane())
+    buf = _pinned.get(key)
+    if buf is None:
+        buf = t.from_numpy(np.empty(arr.shape, dtype=dtype)).pin_memory()
+        _pinned[key] = buf
+    done = _h2d_done.get(key)
+    if done is not None:
+        done.synchronize()
+    np.copyto(buf.numpy(), arr)
+    out = t.empty(arr.shape, dtype=buf.dtype, device="cuda")
+    out.copy_(buf, non_blocking=True)
+    ev = t.cuda.Event()
+    ev.record()
+    _h2d_done[key] = ev
+    return out
+
+
 # ---------------------------------------------------------------------------
 # precision tiers
 

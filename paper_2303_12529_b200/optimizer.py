@@ -296,7 +296,7 @@ def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, mod
         p0 = nv.to_dev(phi0.phi) if phi0 is not None else None
         mdv = nv.to_dev(m) if m is not None else None
     shape = target.shape
-    td = nv.to_dev(target, np.uint8)
+    td = nv.to_dev_staged(target, np.uint8)
     best = nv.empty(shape, np.float64)
     fmask = nv.empty(shape, np.uint8)
     hist = np.zeros((cfg.max_iters + 1, 7))
