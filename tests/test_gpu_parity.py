@@ -480,3 +480,29 @@ def test_reference_kernelset_objects_accepted():
     a = b2.aerial_intensity(m, F, b2.NOMINAL)
     b = b2.aerial_intensity(m, ref_like, b2.NOMINAL)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_clip2048_full_solve_matches_reference(prec):
+    """configs[1] end to end: optimize(iccad_like_clip(0), 24 + 24 kernels,
+    OptConfig()) to the reference's stop rule, against the real reference's
+    own solve (tests/golden/make_clip2048_solve.py, ~35 CPU minutes).
+    fp64: same iteration count, identical final mask and metrics, loss
+    history to rtol 1e-9 (measured: 2e-15, dt and max|v| bit-identical).  fp32: same iteration count and metrics, final
+    mask within a 0.1% flip budget, history to 1e-4."""
+    nv.set_precision(prec)
+    g = golden("clip2048_solve")
+    f, d, F, D = kernels(35, 24, 4)
+    clip = o.iccad_like_clip(0)
+    r = b2.optimize(clip, F, D, b2.OptConfig(precision=prec))
+    ref_mask = np.unpackbits(g["mask_packed"])[:clip.size].reshape(clip.shape)
+    flips = int((r.final_mask != ref_mask).sum())
+    l2, pvb, shots = (int(v) for v in g["metrics"])
+    assert r.iters_run == int(g["iters"])
+    assert (r.metrics.l2, r.metrics.pvband, r.metrics.shots) == (l2, pvb, shots)
+    if prec == "fp64":
+        assert flips == 0
+        assert np.allclose(_hist(r), g["hist"], rtol=1e-9, atol=1e-12)
+    else:
+        assert flips <= 0.001 * clip.sum()
+        assert np.allclose(_hist(r)[:, :3], g["hist"][:, :3], rtol=1e-4)
