@@ -506,3 +506,23 @@ def test_clip2048_full_solve_matches_reference(prec):
     else:
         assert flips <= 0.001 * clip.sum()
         assert np.allclose(_hist(r)[:, :3], g["hist"][:, :3], rtol=1e-4)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("curv", [True, False])
+def test_config1_known_answers(prec, curv):
+    """configs[0] (512^2 two bars, 24 + 24 kernels, default OptConfig) against
+    the known answers the reference produced for SURVEY Appendix A: final-mask
+    sha256 prefix, metrics, iteration count, best L_DSO (6 decimals in fp64)."""
+    import hashlib
+    nv.set_precision(prec)
+    known = {True: ("928b05a5deadb26b", 52, 148, 102, 17, 2657.979594),
+             False: ("74149cbdfadb3b63", 96, 176, 126, 22, 2611.973280)}[curv]
+    t = o.two_bar_512()
+    f, d = b2.gen_synthetic_kernels(35, 24, seed=4)
+    r = b2.optimize(t, f, d, b2.OptConfig(precision=prec, use_curvature=curv))
+    sha = hashlib.sha256(np.ascontiguousarray(r.final_mask.astype(np.uint8)).tobytes()).hexdigest()[:16]
+    assert sha == known[0]
+    assert (r.metrics.l2, r.metrics.pvband, r.metrics.shots, r.iters_run) == known[1:5]
+    best = min(h.l_dso for h in r.loss_history)
+    assert abs(best - known[5]) <= (5e-7 if prec == "fp64" else 1e-5 * known[5])
