@@ -52,7 +52,7 @@ def pvband(z_in, z_out, pitch=1):
 def fracture(mask):
     """Greedy largest-rectangle decomposition, ties topmost then leftmost
     (metrics.py:55-104).  Returns [(x, y, w, h), ...]."""
-    m = np.ascontiguousarray((np.asarray(mask) != 0).astype(np.uint8))
+    m = _as_u8(mask)
     if m.ndim != 2:
         raise ValueError("mask must be 2-D")
     H, W = m.shape
@@ -68,8 +68,21 @@ def fracture(mask):
     return [tuple(int(v) for v in r) for r in buf[:count.value]]
 
 
+def _as_u8(mask):
+    """The mask as contiguous bytes; the native fracture treats any non-zero
+    byte as lit, so uint8 / bool masks pass through without a copy."""
+    a = np.asarray(mask)
+    if a.dtype == np.bool_:
+        a = a.view(np.uint8)
+    elif a.dtype != np.uint8:
+        a = (a != 0).view(np.uint8)
+    return np.ascontiguousarray(a)
+
+
 def shot_count(mask):
-    m = np.ascontiguousarray((np.asarray(mask) != 0).astype(np.uint8))
+    m = _as_u8(mask)
+    if m.ndim != 2:
+        raise ValueError("mask must be 2-D")
     if m.size == 0:
         return 0
     count = ctypes.c_size_t()
