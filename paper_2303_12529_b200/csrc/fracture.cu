@@ -53,11 +53,11 @@ void sweep_run(const int* heights, int a, int b, int y, int* stack, Cand& best) 
   }
 }
 
-// sweep of one bottom row: heights > 0 exactly where the row's mask byte is 1;
-// zero runs are skipped 8 bytes at a time
-Cand sweep_row(const int* heights, const uint8_t* mrow, int W, int y, std::vector<int>& stack) {
+// sweep of columns [x0, W) of one bottom row: heights > 0 exactly where the
+// row's mask byte is 1; zero runs are skipped 8 bytes at a time
+Cand sweep_row(const int* heights, const uint8_t* mrow, int W, int y, std::vector<int>& stack, int x0 = 0) {
   Cand best;
-  int x = 0;
+  int x = x0;
   while (x < W) {
     while (x + 8 <= W) {
       uint64_t w8;
@@ -169,7 +169,26 @@ extern "C" int lsopc_fracture(int H0, int W0, const uint8_t* mask_host, int32_t*
         if (y > ymax) ymax = y;
       }
     }
-    for (int y = best.y; y <= ymax; ++y) rowbest[y] = sweep_row(&hts[(size_t)y * W], &m[(size_t)y * W], W, y, stack);
+    // Re-sweep the affected rows.  Only runs meeting the cleared columns
+    // changed (their heights, or their extent where the rectangle split them):
+    // all lie inside [a, b), the cleared columns widened to the nearest zero
+    // pixel on each side.  A row whose cached best lies outside [a, b) keeps
+    // it as the best of its unchanged runs, so only [a, b) is swept and the
+    // better of the two kept; otherwise the whole row is swept again.
+    for (int y = best.y; y <= ymax; ++y) {
+      const uint8_t* mr = &m[(size_t)y * W];
+      const int* hr = &hts[(size_t)y * W];
+      int a = best.x, b = best.x + best.w;
+      while (a > 0 && mr[a - 1]) --a;
+      while (b < W && mr[b]) ++b;
+      const Cand old = rowbest[y];
+      if (old.area > 0 && (old.x >= b || old.x + old.w <= a)) {
+        const Cand c = sweep_row(hr, mr, b, y, stack, a);
+        rowbest[y] = better(c, old) ? c : old;
+      } else {
+        rowbest[y] = sweep_row(hr, mr, W, y, stack);
+      }
+    }
   }
   *count = k;
   return LSOPC_OK;

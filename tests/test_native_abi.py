@@ -163,3 +163,41 @@ def test_fracture_on_lit_bounding_box_is_translation_exact():
             big[oy:oy + m.shape[0], ox:ox + m.shape[1]] = m
             got = metrics.fracture(big)
             assert got == [(x + ox, y + oy, w, h) for x, y, w, h in ref], (i, oy, ox)
+
+
+def _brute_fracture(mask):
+    """metrics.py:90-104 semantics by exhaustive search: repeatedly clear the
+    largest all-ones rectangle, ties topmost then leftmost."""
+    work = (np.asarray(mask) != 0).astype(np.uint8)
+    H, W = work.shape
+    out = []
+    while True:
+        best = (0, 0, 0, 0, 0)
+        for y in range(H):
+            for x in range(W):
+                if not work[y, x]:
+                    continue
+                for y2 in range(y, H):
+                    for x2 in range(x, W):
+                        if not work[y:y2 + 1, x:x2 + 1].all():
+                            break
+                        a = (y2 - y + 1) * (x2 - x + 1)
+                        if a > best[0] or (a == best[0] and (y < best[2] or (y == best[2] and x < best[1]))):
+                            best = (a, x, y, x2 - x + 1, y2 - y + 1)
+        if best[0] == 0:
+            return out
+        _, x, y, w, h = best
+        out.append((x, y, w, h))
+        work[y:y + h, x:x + w] = 0
+
+
+def test_fracture_incremental_matches_exhaustive_search():
+    """The native fracture re-sweeps only rows (and, when a row's cached best
+    is elsewhere, only the column span) a cleared rectangle can change; an
+    exhaustive search of the reference semantics must agree on random masks."""
+    from paper_2303_12529_b200 import metrics
+    rng = np.random.default_rng(7)
+    for _ in range(120):
+        H, W = (int(v) for v in rng.integers(3, 11, 2))
+        m = (rng.random((H, W)) < rng.choice([0.4, 0.6, 0.8, 0.9])).astype(np.uint8)
+        assert metrics.fracture(m) == _brute_fracture(m)
