@@ -226,6 +226,20 @@ def test_tsdf_bit_exact_golden():
     assert np.array_equal(b2.tsdf_from_mask(t, 20.0, -7.0).phi, g["tsdf_two_rect"])
 
 
+@pytest.mark.parametrize("shape", [(3, 26000), (33000, 3), (3, 33000)])
+def test_tsdf_extreme_shapes_vs_oracle(shape):
+    """Row-pass variants by geometry: rows too wide to stage in shared memory
+    (plain outward scan over the fixed-up g in global memory), and sides over
+    32768 (64-bit squared distances), staged (pruned scan) or not."""
+    rng = np.random.default_rng(shape[0] + 3 * shape[1])
+    for frac in (0.002, 0.5):
+        m = (rng.random(shape) < frac).astype(np.uint8)
+        if m.all() or not m.any():
+            continue
+        for up, lo in ((900.0, -100.0), (1e6, -1e6)):
+            assert np.array_equal(b2.tsdf_from_mask(m, up, lo).phi, o.tsdf(m, up, lo)), (frac, up, lo)
+
+
 @pytest.mark.parametrize("shape", [(7, 13), (64, 64), (100, 37), (512, 512)])
 def test_tsdf_random_vs_oracle(shape):
     rng = np.random.default_rng(shape[0] * 7 + shape[1])
