@@ -28,13 +28,18 @@ constexpr int kSegs = 64;  // row segments per column in the column pass
 // 512 threads beat 256 threads and chunk/near/super 32/32/-, 16/16/-, 16/4/64,
 // 8/8/-, 8/8/64, 8/8/128, 8/4/128, 16/4/128, 16/8/256, 32/4/256, 4/4/64)
 #ifndef LSB_TSDF_CHUNK
-#define LSB_TSDF_CHUNK 8   // columns per chunk minimum (divides 32)
-#define LSB_TSDF_NEAR 4    // offsets scanned column by column before chunk pruning
+#define LSB_TSDF_CHUNK 8  // columns per chunk minimum (divides 32)
+#endif
+#ifndef LSB_TSDF_NEAR
+#define LSB_TSDF_NEAR 4  // offsets scanned column by column before chunk pruning
+#endif
+#ifndef LSB_TSDF_SUPER
 #define LSB_TSDF_SUPER 64  // columns per super-chunk minimum (multiple of the chunk)
 #endif
 #ifndef LSB_TSDF_THREADS
-#define LSB_TSDF_THREADS 512
+#define LSB_TSDF_THREADS 512  // row-pass block size
 #endif
+static_assert(32 % LSB_TSDF_CHUNK == 0 && LSB_TSDF_SUPER % LSB_TSDF_CHUNK == 0, "TSDF chunk geometry");
 
 // phi of a pixel from its exact squared distance (levelset.py:86-101): lit
 // pixels -(d - 0.5), dark pixels d - 0.5, clipped to [d_lower, d_upper]
