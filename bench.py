@@ -39,6 +39,18 @@ K_SIDE, N_K, K_SEED = 35, 24, 4
 METRIC = "ILT iters/s on 2048² clip (24-kernel SOCS); clips/s at 1/2/4/8 B200"
 
 
+DATA = "synthetic (iccad_like_clip per rank, gen_synthetic_kernels(35,24,4))"
+
+
+def workload_config(world):
+    """The `config` of both arms (the precision tier is in `dtype`)."""
+    return {"workload": "2048x2048 iccad_like_clip, SOCS 24+24 kernels K=35, 3 corners, one DSO iteration "
+                        "per step (configs[1]); clip-parallel per GPU (configs[2])",
+            "clip_side": N_SIDE, "kernels_per_set": N_K, "kernel_side": K_SIDE,
+            "parallelism": f"clip-parallel x{world}",
+            "l2_flush": "not needed: per-iteration working set (spectra 768 MiB+) > 126 MB L2"}
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -48,6 +60,8 @@ def parse():
     p.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-solve", action="store_true")
+    p.add_argument("--no-tier", action="store_true", help="skip the other precision tier's sub-line")
+    p.add_argument("--no-config0", action="store_true", help="skip the configs[0] 512^2 sub-line")
     p.add_argument("--clips", type=int, default=64, help="config 3 batch size (0 = skip)")
     p.add_argument("--tile", type=int, default=8192, help="config 5 tile side, split over the ranks (0 = skip)")
     p.add_argument("--tile-iters", type=int, default=6)
@@ -218,6 +232,75 @@ def pass_bytes(n, nk_tot, nsets, prec):
     return [p * n for p in per_px]
 
 
+def time_session(b2, nv, L, sp, focus, defocus, target, K, W, precision, world, dist, sampler=None):
+    """W warm-up + K timed DSO iterations of one on-device session on
+    `target` (stop rule disabled), CUDA events on the session stream, max over
+    ranks.  Returns (ms over the K steps on this rank, max over ranks, the
+    live session, launches per iteration)."""
+    import contextlib
+    import torch
+    from paper_2303_12529_b200 import parallel
+    shape = target.shape
+    fk = focus.device(shape, precision)
+    dk = defocus.device(shape, precision)
+    cfg = b2.OptConfig(max_iters=W + K + 5, stop_patience=10**9, precision=precision)
+    c = b2.optimizer._native_cfg(cfg)
+    td = nv.to_dev(target, np.uint8)
+    sess = ctypes.c_void_p()
+    nv.check(L.lsopc_session_create(fk.plan.handle, fk.handle, dk.handle, nv.ptr(td), None, None,
+                                    ctypes.byref(c), sp, ctypes.byref(sess)))
+    nv.check(L.lsopc_session_enqueue(sess, W))
+    stopped = ctypes.c_int()
+    nv.check(L.lsopc_session_poll(sess, ctypes.byref(stopped), None))
+    launches = L.lsopc_session_launches_per_iter(sess)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with (sampler if sampler is not None else contextlib.nullcontext()):
+        ev0.record(stream)
+        nv.check(L.lsopc_session_enqueue(sess, K))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    nv.check(L.lsopc_session_poll(sess, ctypes.byref(stopped), None))
+    assert not stopped.value, "stop rule fired inside the timed region"
+    return ms, parallel.max_over_ranks(ms, device="cuda"), sess, launches
+
+
+def time_e2e(b2, target, focus, defocus, K, precision, reps=3):
+    """`b2.optimize` from a host uint8 target with K iterations (H2D, TSDF,
+    K iterations, final prints, D2H of best phi + mask, host shot count): one
+    warm-up call, then the median of `reps` (seconds)."""
+    import torch
+    cfg = b2.OptConfig(max_iters=K, stop_patience=10**9, precision=precision)
+    b2.optimize(target, focus, defocus, cfg)
+    times = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = b2.optimize(target, focus, defocus, cfg)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        assert r.iters_run == K
+    return statistics.median(times)
+
+
+def time_solve(b2, target, warm_target, focus, defocus, precision):
+    """Full default `optimize` to the reference's stop rule (configs[1]
+    latency), after one warm-up solve on another target."""
+    import torch
+    b2.optimize(warm_target, focus, defocus, b2.OptConfig(precision=precision))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = b2.optimize(target, focus, defocus, b2.OptConfig(precision=precision))
+    torch.cuda.synchronize()
+    return time.perf_counter() - t0, r
+
+
 def b200_arm(args, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -251,31 +334,9 @@ def b200_arm(args, world, rank, local):
     L = nv.lib()
 
     # ---- device-resident timing: W warm-up + K timed iterations --------------
-    cfg = b2.OptConfig(max_iters=W + K + 5, stop_patience=10**9, precision=args.precision)
-    c = b2.optimizer._native_cfg(cfg)
-    td = nv.to_dev(clip, np.uint8)
-    sess = ctypes.c_void_p()
-    nv.check(L.lsopc_session_create(fk.plan.handle, fk.handle, dk.handle, nv.ptr(td), None, None,
-                                    ctypes.byref(c), sp, ctypes.byref(sess)))
-    nv.check(L.lsopc_session_enqueue(sess, W))
-    stopped = ctypes.c_int()
-    nv.check(L.lsopc_session_poll(sess, ctypes.byref(stopped), None))
-    launches_per_iter = L.lsopc_session_launches_per_iter(sess)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(dev) as clk:
-        ev0.record(stream)
-        nv.check(L.lsopc_session_enqueue(sess, K))
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    nv.check(L.lsopc_session_poll(sess, ctypes.byref(stopped), None))
-    assert not stopped.value, "stop rule fired inside the timed region"
-    ms_max = parallel.max_over_ranks(ms, device="cuda")
+    clk = ClockSampler(dev)
+    ms, ms_max, sess, launches_per_iter = time_session(b2, nv, L, sp, focus, defocus, clip, K, W, args.precision,
+                                                       world, dist, clk)
     value = world * K / (ms_max / 1e3)
 
     # ---- per-pass CUDA-event timing on the session stream (after the timed region)
@@ -295,30 +356,18 @@ def b200_arm(args, world, rank, local):
     dom = max(per_pass, key=lambda w: per_pass[w]["us"])
     iter_s = ms / 1e3 / K
     b_iter = algorithmic_bytes_per_iter(n, 2 * N_K, args.precision)
-    traffic = None
+    traffic = dom_traffic = None
     tpath = ROOT / "profiles" / f"traffic_{args.precision}.json"
     if tpath.exists():
         try:
-            traffic = json.loads(tpath.read_text()).get(str(dom))
+            tj = json.loads(tpath.read_text())
+            traffic = tj.get("iteration")
+            dom_traffic = tj.get(str(dom))
         except Exception:
             traffic = None
 
     # ---- e2e through the public API: host target in, host mask/phi out -------
-    # b2.optimize(host uint8 target) with K iterations: H2D of the target,
-    # TSDF, K iterations, final hard prints, D2H of best phi + final mask, and
-    # the host shot count, all inside the timed call.  One warm-up call, then
-    # the median of 3 (max over ranks).
-    cfg_e2e = b2.OptConfig(max_iters=K, stop_patience=10**9, precision=args.precision)
-    b2.optimize(clip, focus, defocus, cfg_e2e)
-    times = []
-    for _ in range(3):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = b2.optimize(clip, focus, defocus, cfg_e2e)
-        torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
-        assert r.iters_run == K
-    t_e2e = parallel.max_over_ranks(statistics.median(times), device="cuda")
+    t_e2e = parallel.max_over_ranks(time_e2e(b2, clip, focus, defocus, K, args.precision), device="cuda")
     e2e_val = world * K / t_e2e
 
     # ---- config 2: full default solve of this rank's clip (latency) ----------
@@ -326,12 +375,8 @@ def b200_arm(args, world, rank, local):
     if not args.no_solve:
         # warm-up solve on another clip: the first call with a new OptConfig
         # allocates the session buffers and captures the iteration graphs
-        b2.optimize(inputs.iccad_like_clip(seed=1000 + rank), focus, defocus, b2.OptConfig(precision=args.precision))
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        rs = b2.optimize(clip, focus, defocus, b2.OptConfig(precision=args.precision))
-        torch.cuda.synchronize()
-        lat = parallel.max_over_ranks(time.perf_counter() - t0, device="cuda")
+        lat, rs = time_solve(b2, clip, inputs.iccad_like_clip(seed=1000 + rank), focus, defocus, args.precision)
+        lat = parallel.max_over_ranks(lat, device="cuda")
         solve = {"iters": rs.iters_run, "latency_s": round(lat, 4), "wall_time_s": round(rs.wall_time, 4),
                  "l2": rs.metrics.l2, "pvband": rs.metrics.pvband, "shots": rs.metrics.shots,
                  "note": "b2.optimize(iccad_like_clip(rank), OptConfig()) to the reference's stop rule; "
@@ -408,6 +453,49 @@ def b200_arm(args, world, rank, local):
                 "note": f"{T}^2 mosaic of iccad_like_clips, full-height strips over {world} rank(s), "
                         "34-column phi halo exchange + 4 scalar all-reduces per iteration (configs[4])"}
 
+    # ---- the reference's own precision (fp64 tier: complex128 transforms) -----
+    tiers = {}
+    other = "fp64" if args.precision == "fp32" else "fp32"
+    if not args.no_tier:
+        ms_o, ms_o_max, sess_o, _ = time_session(b2, nv, L, sp, focus, defocus, clip, K, W, other, world, dist)
+        L.lsopc_session_destroy(sess_o)
+        b_o = algorithmic_bytes_per_iter(n, 2 * N_K, other)
+        t_o = parallel.max_over_ranks(time_e2e(b2, clip, focus, defocus, K, other), device="cuda")
+        tiers[other] = {"value": round(world * K / (ms_o_max / 1e3), 3), "unit": "iters/s",
+                        "ms_per_step": round(ms_o_max / K, 4),
+                        "dtype": "c128 transforms / f64 level set" if other == "fp64" else
+                                 "c64 transforms / f64 level set",
+                        "e2e": {"value": round(world * K / t_o, 3), "unit": "iters/s"},
+                        "roofline": {"bound": "hbm", "algorithmic_bytes": b_o,
+                                     "achieved": round(b_o / (ms_o / 1e3 / K) / 1e9, 1), "peak": hbm,
+                                     "frac": round(b_o / (ms_o / 1e3 / K) / 1e9 / hbm, 4)}}
+        if not args.no_solve:
+            lat_o, ro = time_solve(b2, clip, inputs.iccad_like_clip(seed=1000 + rank), focus, defocus, other)
+            tiers[other]["solve"] = {"iters": ro.iters_run, "latency_s": round(parallel.max_over_ranks(
+                lat_o, device="cuda"), 4), "l2": ro.metrics.l2, "pvband": ro.metrics.pvband,
+                "shots": ro.metrics.shots}
+        tiers[other]["note"] = (f"same workload as the headline in the {other} tier; device iters/s over {K} "
+                                f"steps, e2e through b2.optimize, full default solve")
+
+    # ---- configs[0]: 512^2 two bars, 24 + 24 kernels, 50 iterations ---------
+    config0 = None
+    if not args.no_config0:
+        bars = inputs.two_bar_layout()
+        c0 = {}
+        for prec in (args.precision, other):
+            ms0, ms0_max, s0, _ = time_session(b2, nv, L, sp, focus, defocus, bars, 50, W, prec, world, dist)
+            L.lsopc_session_destroy(s0)
+            t0e = parallel.max_over_ranks(time_e2e(b2, bars, focus, defocus, 50, prec), device="cuda")
+            lat0, r0 = time_solve(b2, bars, inputs.rect_layout(512, [(100, 100, 80, 300)]), focus, defocus, prec)
+            c0[prec] = {"iters_per_s": round(world * 50 / (ms0_max / 1e3), 2), "ms_per_iter": round(ms0_max / 50, 4),
+                        "e2e_iters_per_s": round(world * 50 / t0e, 2),
+                        "solve": {"iters": r0.iters_run, "latency_s": round(lat0, 4), "l2": r0.metrics.l2,
+                                  "pvband": r0.metrics.pvband, "shots": r0.metrics.shots}}
+        config0 = {"workload": "configs[0]: 512x512 two-bar target (test_acceptance.py:31), 24+24 kernels K=35, "
+                               "OptConfig(max_iters=50, stop_patience=1e9) for iters/s (device: 50 graph-replayed "
+                               "iterations; e2e: b2.optimize from the host target), plus the default solve "
+                               "(reference: 17 iterations, l2 52, pvband 148, shots 102)", **c0}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -424,31 +512,33 @@ def b200_arm(args, world, rank, local):
         "warmup": W, "ms_per_step": round(ms_max / K, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None,
         "dtype": "c64 transforms / f64 level set" if args.precision == "fp32" else "c128 / f64",
-        "data": "synthetic (iccad_like_clip per rank, gen_synthetic_kernels(35,24,4))",
-        "config": {"workload": "2048x2048 iccad_like_clip, SOCS 24+24 kernels K=35, 3 corners, "
-                               "one DSO iteration per step (configs[1]); clip-parallel per GPU (configs[2])",
-                   "clip_side": N_SIDE, "kernels_per_set": N_K, "kernel_side": K_SIDE,
-                   "precision_tier": args.precision, "parallelism": f"clip-parallel x{world}",
-                   "l2_flush": "not needed: per-iteration working set (spectra 768 MiB+) > 126 MB L2"},
+        "data": DATA,
+        "config": workload_config(world),
         "e2e": {"value": round(e2e_val, 3), "unit": "iters/s",
                 "h2d_bytes_per_step": round(n / K), "d2h_bytes_per_step": round(9 * n / K),
                 "note": f"b2.optimize(host uint8 target, max_iters={K}): H2D target, TSDF, {K} iterations, "
                         f"final prints, D2H best phi + mask, host shot count; median of 3 = {t_e2e:.3f} s"},
-        "roofline": {"bound": "hbm", "achieved": round(per_pass[dom]["gbs"], 1), "peak": hbm,
-                     "unit": "GB/s", "frac": round(per_pass[dom]["frac"], 4), "traffic": traffic,
-                     "kernel": per_pass[dom]["name"], "peak_source": src,
+        # the roofline unit is one whole DSO iteration (one graph replay of
+        # its launches): SURVEY §8(d) B_iter = n (64 N_k + 170) B (fp32 tier)
+        # over the measured mean step time; the per-pass table beside it
+        "roofline": {"bound": "hbm", "achieved": round(b_iter / iter_s / 1e9, 1), "peak": hbm,
+                     "unit": "GB/s", "frac": round(b_iter / iter_s / 1e9 / hbm, 4), "traffic": traffic,
+                     "kernel": f"one DSO iteration ({launches_per_iter} launches, CUDA graph)",
+                     "algorithmic_bytes": b_iter,
+                     "algorithmic_bytes_def": "SURVEY.md 8(d): n*(64*N_k + 170) (fp32), n*(128*N_k + 230) (fp64)",
+                     "peak_source": src,
                      "copy_GBps_measured": round(copy_gbs, 1),
-                     "frac_of_copy": round(per_pass[dom]["gbs"] / copy_gbs, 4),
+                     "frac_of_copy": round(b_iter / iter_s / 1e9 / copy_gbs, 4),
+                     "dominant_pass": {"name": per_pass[dom]["name"], "us": round(per_pass[dom]["us"], 2),
+                                       "pass_bytes": pb[dom], "GBps": round(per_pass[dom]["gbs"], 1),
+                                       "frac": round(per_pass[dom]["frac"], 4), "traffic": dom_traffic},
                      "per_pass": {per_pass[w]["name"]: {"us": round(per_pass[w]["us"], 2),
                                                         "GBps": round(per_pass[w]["gbs"], 1),
                                                         "frac": round(per_pass[w]["frac"], 4)}
                                   for w in per_pass},
-                     "iteration": {"algorithmic_bytes_survey": b_iter,
-                                   "achieved_GBps_survey": round(b_iter / iter_s / 1e9, 1),
-                                   "frac_survey": round(b_iter / iter_s / 1e9 / hbm, 4),
-                                   "pass_bytes": sum(pb),
-                                   "achieved_GBps_passes": round(sum(pb) / iter_s / 1e9, 1),
-                                   "frac_passes": round(sum(pb) / iter_s / 1e9 / hbm, 4)}},
+                     "iteration_passes": {"pass_bytes": sum(pb),
+                                          "achieved_GBps_passes": round(sum(pb) / iter_s / 1e9, 1),
+                                          "frac_passes": round(sum(pb) / iter_s / 1e9 / hbm, 4)}},
         "cpu_baseline": cpu,
         "gpu_launches": launches_per_iter * K,
         "clocks": clk.summary(),
@@ -457,32 +547,104 @@ def b200_arm(args, world, rank, local):
         "tile": tile,
         "instant_opc": instant,
         "modulation_search": modsearch,
+        "tiers": tiers,
+        "config0": config0,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def _ref_worker(idx, n_iters, barrier, q):
+    """One single-threaded process of the reference arm: the numpy oracle
+    (the reference algorithm on numpy's own pocketfft, which is single-threaded
+    like the reference) -- untimed setup (spectra, TSDF), then `n_iters` timed
+    DSO iterations on iccad_like_clip(idx) started together with the other
+    processes."""
+    try:
+        sys.path.insert(0, str(ROOT))
+        from oracle import lsopc_oracle as o
+        clip = o.iccad_like_clip(idx)
+        f, d = o.synthetic_kernels(K_SIDE, N_K, K_SEED)
+        hf_f, hf_d = o.spectra(f[0], clip.shape), o.spectra(d[0], clip.shape)
+        cfg = o.Cfg()
+        phi = o.tsdf(clip)
+        barrier.wait()
+        t_start = time.time()
+        g_prev = d_prev = None
+        for it in range(n_iters):
+            mask = o.mask_of(phi).astype(np.float64)
+            prints, _, _, _ = o.forward_losses(mask, clip, f, d, cfg, hf_f, hf_d)
+            g, dd, v, gm = o.step_fields(phi, mask, prints, None, clip, f, d, cfg, g_prev, d_prev,
+                                         g_prev is None, hf_f, hf_d)
+            dt, _ = o.cfl(v, cfg.eta)
+            phi = np.clip(phi + dt * (-v * gm), cfg.d_lower, cfg.d_upper)
+            g_prev, d_prev = g, dd
+        q.put((idx, t_start, time.time(), None))
+    except BaseException as e:  # report, never hang the parent
+        try:
+            barrier.abort()
+        except Exception:
+            pass
+        q.put((idx, 0.0, 0.0, repr(e)))
+
+
+def ref_processes(K):
+    """P = min(cores, floor(0.8 RAM / 10 GB)) (one
+    2048^2 oracle process peaks at ~9.8 GB), each running ceil(K / P)
+    iterations so that at least K are timed."""
+    cores = os.cpu_count() or 1
+    try:
+        import psutil
+        ram = psutil.virtual_memory().total
+    except Exception:
+        ram = 64 << 30
+    pmax = max(1, min(cores, int(0.8 * ram / (10 << 30))))
+    pmax = int(os.environ.get("BENCH_REF_PROCS", pmax))
+    p = max(1, min(pmax, K))
+    return p, -(-K // p)
+
+
 def reference_arm(args, world, rank):
+    """The reference's CPU implementation of the path on this box's host
+    cores: P concurrent single-threaded processes of the numpy oracle (the
+    reference is single-threaded numpy; independent runs may execute
+    concurrently), each on its own clip, started together after
+    an untimed setup; value = all timed iterations / wall time from the first
+    start to the last finish."""
     if rank != 0:
         return
+    import multiprocessing as mp
     K = args.steps
-    budget_s = float(os.environ.get("BENCH_REF_BUDGET_S", "150"))
-    times, thr = cpu_iteration_sample(1)
-    n_more = max(0, min(K, int(budget_s / max(times[0], 1e-3))) - 1)
-    if n_more:
-        t2, _ = cpu_iteration_sample(n_more + 1)
-        times = t2
-    v = len(times) / sum(times)
-    sample = (f"{len(times)} full DSO iteration(s) of the numpy oracle port (reference algorithm, "
-              f"pocketfft via scipy.fft on {thr} threads), iccad_like_clip(0) 2048^2, N_k=24; "
-              f"requested steps={K}, bounded to ~{budget_s:.0f} s")
+    P, n_each = ref_processes(K)
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
+    ctx = mp.get_context("spawn")
+    barrier = ctx.Barrier(P)
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ref_worker, args=(i, n_each, barrier, q)) for i in range(P)]
+    for pr in procs:
+        pr.start()
+    res = [q.get() for _ in procs]
+    for pr in procs:
+        pr.join()
+    errs = [r[3] for r in res if r[3]]
+    if errs:
+        raise RuntimeError(f"reference worker failed: {errs[0]}")
+    wall = max(r[2] for r in res) - min(r[1] for r in res)
+    total = P * n_each
+    v = total / wall
+    sample = (f"{P} concurrent single-threaded processes x {n_each} full DSO iteration(s) each of the numpy "
+              f"oracle (reference algorithm, numpy pocketfft), iccad_like_clip(0..{P - 1}) 2048^2, N_k=24+24; "
+              f"spectra + TSDF untimed; wall {wall:.1f} s")
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "iters/s",
-            "n_gpus": world, "steps": len(times), "warmup": 0, "ms_per_step": round(1e3 / v, 1),
+            "n_gpus": world, "steps": total, "warmup": 0, "ms_per_step": round(1e3 / v, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 / f64",
-            "data": "synthetic", "config": {"workload": "2048x2048 iccad_like_clip, SOCS 24+24, one DSO iteration"},
-            "cpu_baseline": {"value": round(v, 5), "unit": "iters/s", "cores": thr, "kind": "port",
+            "data": DATA, "config": workload_config(world),
+            "cpu_baseline": {"value": round(v, 5), "unit": "iters/s", "cores": P, "kind": "port",
                              "sample": sample},
+            "clips_per_s_derived": round(v / 25.0, 6),
+            "clips_note": "configs[2] CPU clips/s = iters/s / 25 (the configs[1] solve takes 25 iterations)",
             "e2e": {"value": round(v, 5), "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

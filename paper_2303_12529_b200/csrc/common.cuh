@@ -59,6 +59,12 @@ LS_D uint32_t row_of(const RowSplit& r, size_t i) {
 // deterministic reductions: warp shuffle -> smem -> one value per block; the
 // per-block partials are combined later by a single block in fixed order.
 
+// NaN-propagating max / clamp: numpy's np.max, np.maximum and np.clip return
+// NaN when an operand is NaN, where fmax / fmin drop it (litho.py:126,
+// optimizer.py:148,262-268 on non-finite fields).
+LS_HD double nmax(double a, double b) { return (a > b || a != a) ? a : b; }
+LS_HD double nclip(double x, double lo, double hi) { return x != x ? x : fmin(fmax(x, lo), hi); }
+
 template <typename T> LS_D T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -66,7 +72,7 @@ template <typename T> LS_D T warp_sum(T v) {
 }
 template <typename T> LS_D T warp_max(T v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) v = nmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 

@@ -21,7 +21,7 @@ LS_D void reduce_partials(const double* part, int nb, double (&out)[NV], double*
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const double p = __ldcg(part + NV * b + j);
-      acc[j] = MAX ? fmax(acc[j], p) : acc[j] + p;
+      acc[j] = MAX ? nmax(acc[j], p) : acc[j] + p;
     }
   }
   if (MAX) block_max<NV>(acc, red);

@@ -223,8 +223,8 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       if (x + e >= tl.ix0 && x + e < tl.ix1) {
-        mx[0] = fmax(mx[0], fabs(vt[e]));
-        mx[1] = fmax(mx[1], gm[e]);
+        mx[0] = nmax(mx[0], fabs(vt[e]));
+        mx[1] = nmax(mx[1], gm[e]);
       }
     }
   }
@@ -255,10 +255,10 @@ k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const doubl
   auto one = [&](double ph, double uu, double gg, double& step) {
     if (gm) {  // optimizer.py:329: phi - dt * v_total * grad_mag
       step = mul(mul(dt, uu), gg);
-      return fmin(fmax(sub(ph, step), lo), hi);
+      return nclip(sub(ph, step), lo, hi);
     }
     step = mul(dt, uu);  // optimizer.py:262,266: phi + dt * (-v_total * grad_mag)
-    return fmin(fmax(add(ph, step), lo), hi);
+    return nclip(add(ph, step), lo, hi);
   };
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n4; q += (size_t)gridDim.x * blockDim.x) {
     const size_t i = 4 * q;
@@ -277,7 +277,7 @@ k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const doubl
       *reinterpret_cast<double2*>(phi + i) = make_double2(q0, q1);
       *reinterpret_cast<double2*>(phi + i + 2) = make_double2(q2, q3);
       *reinterpret_cast<uchar4*>(mask + i) = make_uchar4(q0 <= 0.0, q1 <= 0.0, q2 <= 0.0, q3 <= 0.0);
-      mx[0] = fmax(fmax(fmax(mx[0], fabs(s0)), fmax(fabs(s1), fabs(s2))), fabs(s3));
+      mx[0] = nmax(nmax(nmax(mx[0], fabs(s0)), nmax(fabs(s1), fabs(s2))), fabs(s3));
     } else {
       for (int e = 0; e < 4; ++e) {
         if (x + e < tl.ix0 || x + e >= tl.ix1) continue;  // strip halo: owned by a neighbour rank
@@ -285,7 +285,7 @@ k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const doubl
         const double p = one(phi[i + e], u[i + e], gm ? gm[i + e] : 0.0, step);
         phi[i + e] = p;
         mask[i + e] = p <= 0.0;
-        mx[0] = fmax(mx[0], fabs(step));
+        mx[0] = nmax(mx[0], fabs(step));
       }
     }
   }
@@ -341,7 +341,7 @@ __global__ void k_elementwise(int op, size_t n, const double* __restrict__ a, co
       case EW_CG: out[i] = add(-a[i], mul(p0, b[i])); break;        // optimizer.py:335
       case EW_MOTION: out[i] = mul(-a[i], b[i]); break;             // optimizer.py:140 (-v |grad phi|)
       case EW_EVOLVE:                                                // levelset.py:165
-        out[i] = fmin(fmax(add(a[i], mul(p0, b[i])), p1), p2); break;
+        out[i] = nclip(add(a[i], mul(p0, b[i])), p1, p2); break;
       case EW_AHF:                                                   // levelset.py:151
         out[i] = mul(0.5, add(1.0, mul(2.0 / CUDART_PI, atan(dvd(a[i], p0))))); break;
       case EW_HYPOT: out[i] = np_hypot(a[i], b[i]); break;          // levelset.py:62
@@ -356,7 +356,7 @@ __global__ void k_elementwise(int op, size_t n, const double* __restrict__ a, co
 __global__ void k_dsn_init(size_t n, const float* __restrict__ phi_raw, const float* __restrict__ m_raw,
                            double lo, double hi, double eps, double* phi0, double* m) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    phi0[i] = fmin(fmax((double)phi_raw[i], lo), hi);
+    phi0[i] = nclip((double)phi_raw[i], lo, hi);
     m[i] = mul(0.5, add(1.0, mul(2.0 / CUDART_PI, atan(dvd((double)m_raw[i], eps)))));
   }
 }
@@ -371,7 +371,7 @@ k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restric
       case RD_SUMSQDIFF: { double t = a[i] - b[i]; acc[0] += t * t; } break;
       case RD_DOT: acc[0] += a[i] * b[i]; break;
       case RD_DOTDIFF: acc[0] += a[i] * (a[i] - b[i]); break;
-      case RD_MAXABS: acc[0] = fmax(acc[0], fabs(a[i])); break;
+      case RD_MAXABS: acc[0] = nmax(acc[0], fabs(a[i])); break;
       case RD_COUNTNEQ8:  // b8 null: vs 0; W > 0: columns [ix0, ix1) only
         if (W > 0) {
           const int x = (int)col_of(row_split(W), i);

@@ -84,10 +84,15 @@ struct lsopc_plan {
                       &scal, &hard, &tsdf_i, &tsdf_f})
       b->release();
   }
+  // bumped whenever T or A is reallocated: CUDA graphs captured before that
+  // hold the old pointers and must be re-captured (lsopc_session::gen)
+  unsigned long long gen = 0;
   size_t n() const { return g.n(); }
   void ensure_T(int nk_total) {
-    T.ensure((size_t)nk_total * n() * g.csize());
-    A.ensure((size_t)nk_total * n() * g.csize());
+    const size_t bytes = (size_t)nk_total * n() * g.csize();
+    if (bytes > T.cap || bytes > A.cap) ++gen;
+    T.ensure(bytes);
+    A.ensure(bytes);
   }
 };
 
@@ -433,11 +438,17 @@ struct lsopc_session {
   DevBuf scalars;  // 8 doubles exchanged with the other ranks between phases
   // one DSO iteration captured as a CUDA graph per buffer parity (it & 1)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  unsigned long long gen = 0;  // plan->gen when the graphs were captured
   int* hflag = nullptr;  // pinned host copies of DevState::stopped (async polling)
   cudaEvent_t ev[2] = {nullptr, nullptr};
-  ~lsopc_session() {
-    for (auto& g : graph)
+  void drop_graphs() {
+    for (auto& g : graph) {
       if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  }
+  ~lsopc_session() {
+    drop_graphs();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (hflag) cudaFreeHost(hflag);
@@ -616,6 +627,32 @@ void enqueue_phase(lsopc_session* ss, int phase, cudaStream_t s) {
   ck_launch("dso phase");
 }
 
+// Capture one DSO iteration per buffer parity as a CUDA graph (on a private
+// stream: the caller's may be the legacy stream).  The graphs bake in the
+// plan's T / A pointers, so they are tied to the plan's buffer generation.
+void capture_graphs(lsopc_session* ss) {
+  ss->drop_graphs();
+  const char* ng = std::getenv("LSOPC_B200_NO_GRAPH");
+  if (ng && ng[0] == '1') return;
+  cudaStream_t cs;
+  ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
+  for (int par = 0; par < 2; ++par) {
+    cudaGraph_t gr;
+    ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed), "capture");
+    enqueue_iteration(ss, par, cs);
+    ck(cudaStreamEndCapture(cs, &gr), "capture end");
+    ck(cudaGraphInstantiate(&ss->graph[par], gr, 0), "graph instantiate");
+    cudaGraphDestroy(gr);
+  }
+  cudaStreamDestroy(cs);
+  ss->gen = ss->plan->gen;
+}
+
+// graphs of a session whose plan buffers moved since capture are re-captured
+void refresh_graphs(lsopc_session* ss) {
+  if (ss->gen != ss->plan->gen && (ss->graph[0] || ss->graph[1])) capture_graphs(ss);
+}
+
 }  // namespace
 
 extern "C" {
@@ -644,6 +681,9 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
       ss->s = s;
       ss->it = 0;
       ss->have_mod = mod_dev != nullptr;
+      ss->tiled = false;  // a pooled strip session comes back as a whole-grid one
+      ss->tile = Tile{};
+      plan->ensure_T(focus->nk + defocus->nk);
       if (fresh) {
         ss->target.ensure(n);
         ss->phi.ensure(n * 8);
@@ -661,7 +701,6 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
         ss->part_up.ensure((size_t)ls_blocks() * sizeof(double));
         ss->dots.ensure((size_t)(finish_max_blocks() + 1) * 2 * sizeof(double));
         if (mod_dev) ss->mod.ensure(n * 8);
-        plan->ensure_T(focus->nk + defocus->nk);
       }
       ck(cudaMemcpyAsync(ss->target.p, target_dev, n, cudaMemcpyDeviceToDevice, s), "memcpy");
       // optimizer.py:197-201: uniform target -> DegenerateInputError
@@ -687,21 +726,8 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
       ck(cudaMemcpyAsync(ss->state.p, &h, sizeof(h), cudaMemcpyHostToDevice, s), "memcpy");
       for (int i = 0; i < 2; ++i) ck(cudaMemsetAsync(ss->v[i].p, 0, n * 8, s), "memset");
       ck(cudaStreamSynchronize(s), "sync");
-      // capture the two parities on a private stream (the caller's may be the legacy stream)
-      const char* ng = std::getenv("LSOPC_B200_NO_GRAPH");
-      if (fresh && !(ng && ng[0] == '1')) {
-      cudaStream_t cs;
-      ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
-      for (int par = 0; par < 2; ++par) {
-        cudaGraph_t gr;
-        ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed), "capture");
-        enqueue_iteration(ss, par, cs);
-        ck(cudaStreamEndCapture(cs, &gr), "capture end");
-        ck(cudaGraphInstantiate(&ss->graph[par], gr, 0), "graph instantiate");
-        cudaGraphDestroy(gr);
-      }
-      cudaStreamDestroy(cs);
-      }
+      if (fresh) capture_graphs(ss);
+      else refresh_graphs(ss);  // a pooled session whose plan buffers were reallocated
       if (fresh) {
         ck(cudaHostAlloc(&ss->hflag, 2 * sizeof(int), cudaHostAllocDefault), "host alloc");
         for (auto& e : ss->ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -717,6 +743,7 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
 int lsopc_session_enqueue(lsopc_session* ss, int n) {
   return guarded([&] {
     if (!ss) throw Error(LSOPC_EINVAL, "null session");
+    refresh_graphs(ss);  // another call on this plan may have grown T / A meanwhile
     for (int i = 0; i < n && ss->it < ss->cfg.max_iters; ++i) {
       if (ss->graph[ss->it & 1]) ck(cudaGraphLaunch(ss->graph[ss->it & 1], ss->s), "graph launch");
       else enqueue_iteration(ss, ss->it & 1, ss->s);

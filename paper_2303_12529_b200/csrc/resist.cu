@@ -38,9 +38,9 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     // litho.py:125-126: I = max(dose * sum, 0); corners: litho.py:147-149
     double sf = (double)If[i];
-    double i_nom = fmax(1.0 * sf, 0.0);
-    double i_out = fmax(1.02 * sf, 0.0);
-    double i_in = Id ? fmax(0.98 * (double)Id[i], 0.0) : 0.0;
+    double i_nom = nmax(1.0 * sf, 0.0);
+    double i_out = nmax(1.02 * sf, 0.0);
+    double i_in = Id ? nmax(0.98 * (double)Id[i], 0.0) : 0.0;
     if (h_nom) {  // litho.py:129-131 (inclusive threshold)
       h_nom[i] = i_nom >= p.i_th;
       h_out[i] = i_out >= p.i_th;
@@ -132,9 +132,9 @@ k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, con
     // API path (print_corners / ilt_loss) on the same intensities
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const double i_nom = fmax(1.0 * (double)sf[e], 0.0);
-      const double i_out = fmax(1.02 * (double)sf[e], 0.0);
-      const double i_in = Id ? fmax(0.98 * (double)sd[e], 0.0) : 0.0;
+      const double i_nom = nmax(1.0 * (double)sf[e], 0.0);
+      const double i_out = nmax(1.02 * (double)sf[e], 0.0);
+      const double i_in = Id ? nmax(0.98 * (double)sd[e], 0.0) : 0.0;
       const double zn = sigmoid(i_nom, p.i_th, p.sigma_z), zo = sigmoid(i_out, p.i_th, p.sigma_z),
                    zi = sigmoid(i_in, p.i_th, p.sigma_z);
       const double dn = zn - zt[e], di = zi - zt[e], dout = zo - zt[e];
@@ -164,7 +164,7 @@ k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, con
 template <typename R>
 __global__ void k_scale_intensity(size_t n, const R* __restrict__ I, double dose, double* out) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    out[i] = fmax(dose * (double)I[i], 0.0);
+    out[i] = nmax(dose * (double)I[i], 0.0);
 }
 
 template <typename R>

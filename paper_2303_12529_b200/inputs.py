@@ -63,6 +63,8 @@ def rect_layout(side, rects):
 
 
 def two_bar_layout():
+    """parse_layout("SIZE 512\\nRECT 150 120 70 270\\nRECT 290 120 70 270\\n"):
+    BASELINE configs[0] (test_acceptance.py:31)."""
     return rect_layout(512, [(150, 120, 70, 270), (290, 120, 70, 270)])
 
 

@@ -240,6 +240,21 @@ def _native_cfg(cfg, max_iters=None, stop_patience=None, use_curvature=None, upd
     return c
 
 
+def _precision(cfg):
+    """The transform tier of a config; reference OptConfigs have no
+    `precision` field and take the package default."""
+    return getattr(cfg, "precision", None)
+
+
+def _check_kernel_sets(shape, focus_kernels, defocus_kernels):
+    for ks, sel in ((focus_kernels, "focus"), (defocus_kernels, "defocus")):
+        if ks.side > min(shape):
+            raise ValueError(f"kernel side {ks.side} exceeds grid {shape}")
+        if ks.condition != sel:
+            raise ValueError(f"kernel set condition {ks.condition!r} does not match "
+                             f"process condition {sel!r}")
+
+
 def _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation):
     target = _check_target(target)
     shape = target.shape
@@ -252,13 +267,8 @@ def _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation):
             raise ValueError("modulation dimensions do not match target")
         if m.size and (m.min() < 0 or m.max() > 1):
             raise ValueError("modulation values must lie in [0, 1]")
-    for ks, sel in ((focus_kernels, "focus"), (defocus_kernels, "defocus")):
-        if ks.side > min(shape):
-            raise ValueError(f"kernel side {ks.side} exceeds grid {shape}")
-        if ks.condition != sel:
-            raise ValueError(f"kernel set condition {ks.condition!r} does not match "
-                             f"process condition {sel!r}")
-    prec = cfg.precision
+    _check_kernel_sets(shape, focus_kernels, defocus_kernels)
+    prec = _precision(cfg)
     fk = litho.device_kernels(focus_kernels, shape, prec)
     dk = litho.device_kernels(defocus_kernels, shape, prec)
     return target, m, fk, dk
@@ -268,12 +278,39 @@ def _is_device_tensor(x):
     return x is not None and hasattr(x, "is_cuda") and x.is_cuda
 
 
-def _device_f64(x, shape):
+def _device_f64(x, shape, what):
     if x is None:
         return None
     if tuple(x.shape) != tuple(shape):
-        raise ValueError("device initial state does not match the target shape")
+        raise ValueError(f"{what} dimensions do not match target")
     return x.to(dtype=nv.torch().float64).contiguous()
+
+
+def _device_inputs(target, focus_kernels, defocus_kernels, cfg, phi0, modulation):
+    """`_prepare` for a device-resident initial state (DevelSet-Net front end,
+    dsn.py, which has already clipped phi0 and mapped m through the AHF on the
+    device).  The other input may be a host array / LevelSetField: it is
+    validated like `optimize` validates it (optimizer.py:215-228) and
+    uploaded, so mixed input kinds behave like all-host ones."""
+    target = _check_target(target)
+    shape = target.shape
+    _check_kernel_sets(shape, focus_kernels, defocus_kernels)
+    if phi0 is not None and not _is_device_tensor(phi0):
+        p = phi0.phi if hasattr(phi0, "phi") else _f64(phi0)
+        if p.shape != shape:
+            raise ValueError("phi0 dimensions do not match target")
+        phi0 = nv.to_dev(p)
+    if modulation is not None and not _is_device_tensor(modulation):
+        m = _f64(modulation)
+        if m.shape != shape:
+            raise ValueError("modulation dimensions do not match target")
+        if m.size and (m.min() < 0 or m.max() > 1):
+            raise ValueError("modulation values must lie in [0, 1]")
+        modulation = nv.to_dev(m)
+    prec = _precision(cfg)
+    fk = litho.device_kernels(focus_kernels, shape, prec)
+    dk = litho.device_kernels(defocus_kernels, shape, prec)
+    return target, fk, dk, _device_f64(phi0, shape, "phi0"), _device_f64(modulation, shape, "modulation")
 
 
 def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=None):
@@ -283,14 +320,7 @@ def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, mod
     clip's device loop)."""
     t0 = time.perf_counter()
     if _is_device_tensor(phi0) or _is_device_tensor(modulation):
-        # device-resident initial state (DevelSet-Net front end, dsn.py): the
-        # caller has already clipped phi0 and mapped m through the AHF on the device
-        target = _check_target(target)
-        fk = litho.device_kernels(focus_kernels, target.shape, cfg.precision)
-        dk = litho.device_kernels(defocus_kernels, target.shape, cfg.precision)
-        m = None
-        p0 = _device_f64(phi0, target.shape)
-        mdv = _device_f64(modulation, target.shape)
+        target, fk, dk, p0, mdv = _device_inputs(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
     else:
         target, m, fk, dk = _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
         p0 = nv.to_dev(phi0.phi) if phi0 is not None else None

@@ -69,7 +69,7 @@ def gather_records(records, group=None):
 
 
 def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, solver=None,
-                   synchronize=None, lanes=2):
+                   synchronize=None, lanes=2, results=None):
     """Solve every clip of `targets` (a sequence of 2-D uint8 layouts; a
     `LazyClips` lets each rank generate only its own clips) on the rank that
     owns it.  Returns (records of all clips ordered by index,
@@ -77,7 +77,8 @@ def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, sol
 
     `solver(target, focus, defocus, cfg) -> OptimizationResult` replaces the
     device loop (tests inject a stub).  Without it, `lanes` concurrent
-    streams each solve every lanes-th clip of this rank's shard.
+    streams each solve every lanes-th clip of this rank's shard.  `results`
+    (a dict, optional) receives this rank's OptimizationResult per clip index.
     """
     rank, world = world_info(group)
     mine = [(i, targets[i]) for i in shard(len(targets), rank, world)]  # inputs built before timing
@@ -87,6 +88,8 @@ def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, sol
     records = []
 
     def record(i, r):
+        if results is not None:
+            results[i] = r
         m = r.metrics
         records.append(ClipRecord(i, rank, int(m.l2), int(m.pvband), int(m.shots), int(r.iters_run),
                                   float(r.wall_time)))

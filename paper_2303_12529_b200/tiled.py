@@ -123,9 +123,17 @@ def all_reduce_(t, op):
     return t
 
 
-def exchange_halos(phi, strip):
+def exchange_halos(phi, strip, tags=True):
     """Refresh the HALO columns on each side of the interior of `phi`
-    (H x ww torch tensor) from the neighbouring ranks' interiors (wrapping)."""
+    (H x ww torch tensor) from the neighbouring ranks' interiors (wrapping).
+
+    NCCL ignores P2P tags and pairs the operations between two ranks by
+    position, so the order below is what keeps the two messages apart when
+    left == right (two ranks): each rank sends its left edge first and its
+    right edge second, and receives from its right neighbour first (that
+    neighbour's left edge) and from its left neighbour second.  With distinct
+    neighbours the order is immaterial.  `tags=False` exercises that
+    positional matching on backends that honour tags (gloo)."""
     dist = _dist()
     if strip.world == 1:
         return
@@ -139,9 +147,9 @@ def exchange_halos(phi, strip):
     send_r = stage(phi[:, i1 - h:i1].contiguous())    # -> right neighbour's left halo
     recv_l = torch.empty_like(send_l)
     recv_r = torch.empty_like(send_r)
-    # tags keep the two messages apart when left == right (two ranks)
-    ops = [dist.P2POp(dist.isend, send_l, left, tag=1), dist.P2POp(dist.isend, send_r, right, tag=2),
-           dist.P2POp(dist.irecv, recv_l, left, tag=2), dist.P2POp(dist.irecv, recv_r, right, tag=1)]
+    t1, t2 = (1, 2) if tags else (0, 0)
+    ops = [dist.P2POp(dist.isend, send_l, left, tag=t1), dist.P2POp(dist.isend, send_r, right, tag=t2),
+           dist.P2POp(dist.irecv, recv_r, right, tag=t1), dist.P2POp(dist.irecv, recv_l, left, tag=t2)]
     for req in dist.batch_isend_irecv(ops):
         req.wait()
     phi[:, i0 - h:i0].copy_(recv_l)
@@ -177,7 +185,7 @@ def optimize_tiled(target, focus_kernels, defocus_kernels, cfg, phi0=None):
     cols = st.columns()
     i0, i1 = st.interior
     xlo, xhi = st.stencil_bounds()
-    prec = cfg.precision
+    prec = getattr(cfg, "precision", None)
 
     # initial level set: the whole tile's TSDF (levelset.py:86-101) or phi0, windowed
     if phi0 is None:

@@ -540,3 +540,79 @@ def test_config1_known_answers(prec, curv):
     assert (r.metrics.l2, r.metrics.pvband, r.metrics.shots, r.iters_run) == known[1:5]
     best = min(h.l_dso for h in r.loss_history)
     assert abs(best - known[5]) <= (5e-7 if prec == "fp64" else 1e-5 * known[5])
+
+
+@pytest.mark.parametrize("prec_name", ["fp64", "fp32"])
+def test_optimize_batch_two_lanes_matches_sequential(prec_name):
+    """configs[2] batch path: two lanes (threads with their own CUDA stream,
+    work buffers and spectra) solving alternate clips give every clip's
+    sequential `optimize` result bit for bit -- histories, final masks and
+    metrics."""
+    from paper_2303_12529_b200 import parallel
+    nv.set_precision(prec_name)
+    f, d, F, D = kernels(17, 4, 1)
+    clips = [o.iccad_like_clip(seed=s, n=256, n_wires=6, lo=32, hi=224, wmin=10, wmax=20, lmin=40, lmax=120,
+                                spacing=10) for s in range(6)]
+    cfg = b2.OptConfig(max_iters=12, precision=prec_name)
+    seq = [b2.optimize(c, F, D, cfg) for c in clips]
+    got = {}
+    recs, secs = parallel.optimize_batch(clips, F, D, cfg, lanes=2, results=got)
+    assert sorted(got) == list(range(6)) and [r.index for r in recs] == list(range(6))
+    for i, r in enumerate(seq):
+        g = got[i]
+        assert np.array_equal(_hist(g), _hist(r)), i
+        assert np.array_equal(g.final_mask, r.final_mask), i
+        assert np.array_equal(g.final_phi.phi, r.final_phi.phi), i
+        assert (recs[i].l2, recs[i].pvband, recs[i].shots, recs[i].iters) == \
+            (r.metrics.l2, r.metrics.pvband, r.metrics.shots, r.iters_run), i
+
+
+def test_pooled_session_survives_work_buffer_growth():
+    """a pooled session's captured graphs bake in the
+    plan's per-kernel work buffers; a larger kernel set on the same grid grows
+    (reallocates) them.  optimize(4+4) -> optimize(24+24) -> optimize(4+4)
+    must give the first result again, not replay a graph on freed memory."""
+    nv.set_precision("fp32")
+    f4, d4, F4, D4 = kernels(17, 4, 1)
+    f24, d24, F24, D24 = kernels(17, 24, 1)
+    t = o.rect_layout(128, [(25, 30, 30, 50), (70, 60, 40, 40)])
+    cfg = b2.OptConfig(max_iters=8, stop_patience=10**9)
+    r1 = b2.optimize(t, F4, D4, cfg)
+    b2.optimize(t, F24, D24, cfg)
+    b2.aerial_intensity(t.astype(np.float64), F24, b2.NOMINAL)
+    r3 = b2.optimize(t, F4, D4, cfg)
+    assert np.array_equal(_hist(r1), _hist(r3))
+    assert np.array_equal(r1.final_phi.phi, r3.final_phi.phi)
+
+
+def test_nan_propagates_like_numpy():
+    """np.max / np.maximum / np.clip return NaN on NaN
+    operands; the device max reductions and clamps do the same."""
+    v = np.ones((8, 8))
+    v[3, 4] = np.nan
+    dt, conv = b2.cfl_timestep(v, 0.85)
+    assert np.isnan(dt) and conv is False
+    f, d, F, D = kernels(5, 2, 0)
+    m = np.zeros((16, 16))
+    m[4:9, 5:12] = 1.0
+    m[2, 2] = np.nan
+    assert np.isnan(b2.aerial_intensity(m, F, b2.NOMINAL)).all()  # np.maximum(NaN, 0) = NaN
+
+
+def test_device_initial_state_validates_like_host():
+    """a device phi0 takes the same kernel-set checks as a
+    host one, and mixing a device phi0 with a host modulation works."""
+    import torch
+    nv.set_precision("fp64")
+    f, d, F, D = kernels(9, 2, 0)
+    t = o.rect_layout(64, [(10, 12, 20, 30)])
+    phi0 = b2.tsdf_from_mask(t)
+    dev_phi = torch.as_tensor(phi0.phi, device="cuda")
+    with pytest.raises(ValueError):
+        b2.optimize(t, D, F, b2.OptConfig(max_iters=2), phi0=dev_phi)  # swapped conditions
+    m = np.full(t.shape, 0.5)
+    r_host = b2.optimize(t, F, D, b2.OptConfig(max_iters=4), phi0=phi0, modulation=m)
+    r_mix = b2.optimize(t, F, D, b2.OptConfig(max_iters=4), phi0=dev_phi, modulation=m)
+    assert np.array_equal(_hist(r_host), _hist(r_mix))
+    with pytest.raises(ValueError):
+        b2.optimize(t, F, D, b2.OptConfig(max_iters=2), phi0=dev_phi, modulation=np.full(t.shape, 2.0))

@@ -1,0 +1,100 @@
+"""Tall / wide geometries against the oracle.
+
+8192-point columns (8192 x 256) take the float32 spectra build above 4096,
+the 4-CTA cluster column passes (`k_pass_cluster`) and the four-step F1
+split (`k_f1_split`); 8192-point rows (256 x 8192) take the tall-row TMA
+row passes.  Everything is checked against the numpy oracle on the same
+inputs with the production kernel model (24 + 24 kernels, K = 35, seed 4):
+
+  intensity (3 corners)      rel-to-max 1e-5   (litho.py:114-126)
+  soft prints                abs 1e-5          (litho.py:141-154)
+  ILT / PVB gradients        rel-to-max 2e-5   (optimizer.py:99-129)
+  6-iteration optimize       history rtol 1e-4 (optimizer.py:204-284)
+
+fp32 tier (the fp64 tier stops at 4096-point sides).  The oracle runs on
+the host's cores through scipy.fft (same pocketfft as numpy).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import lsopc_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+b2 = pytest.importorskip("paper_2303_12529_b200")
+from paper_2303_12529_b200 import _native as nv  # noqa: E402
+
+SHAPES = [(8192, 256), (256, 8192)]
+
+
+def strip_layout(shape, seed, n=40):
+    """Random Manhattan rectangles 30-120 px on a tall or wide strip."""
+    rng = np.random.default_rng(seed)
+    t = np.zeros(shape, np.uint8)
+    H, W = shape
+    for _ in range(n):
+        h, w = rng.integers(30, 120, size=2)
+        y, x = rng.integers(0, H - h), rng.integers(0, W - w)
+        t[y:y + h, x:x + w] = 1
+    return t
+
+
+@pytest.fixture(scope="module")
+def model():
+    f, d = o.synthetic_kernels(35, 24, 4)
+    F = b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(*f)], "focus")
+    D = b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(*d)], "defocus")
+    return f, d, F, D
+
+
+@pytest.fixture(autouse=True)
+def fp32_and_threads():
+    old = nv.get_precision()
+    nv.set_precision("fp32")
+    o.use_threads(os.cpu_count() or 1)
+    yield
+    o.use_threads(None)
+    nv.set_precision(old)
+
+
+def relmax(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / np.abs(b).max()
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_tall_forward_and_gradients_vs_oracle(model, shape):
+    f, d, F, D = model
+    t = strip_layout(shape, sum(shape))
+    m = t.astype(np.float64)
+    hf_f, hf_d = o.spectra(f[0], shape), o.spectra(d[0], shape)
+    for arrs, ks, cond, hf in ((f, F, b2.NOMINAL, hf_f), (f, F, b2.OUTER, hf_f), (d, D, b2.INNER, hf_d)):
+        out = b2.aerial_intensity(m, ks, cond)
+        ref = o.intensity(m, arrs[0], arrs[1], cond.dose, hf)
+        assert relmax(out, ref) <= 1e-5, (shape, cond.label)
+    cfg = b2.OptConfig()
+    p = b2.print_corners(m, F, D, cfg, binarize=False)
+    pr = o.corners(m, f, d, binarize=False, hf_focus=hf_f, hf_defocus=hf_d)
+    for c in ("nominal", "inner", "outer"):
+        assert np.abs(getattr(p, c) - pr[c]).max() <= 1e-5, (shape, c)
+    gi = b2.ilt_gradient(m, pr["nominal"], t, F, cfg)
+    gp = b2.pvb_gradient(m, pr["inner"], pr["outer"], t, F, D, cfg)
+    assert relmax(gi, o.ilt_grad(m, pr["nominal"], t, f, hf=hf_f)) <= 2e-5, shape
+    assert relmax(gp, o.pvb_grad(m, pr["inner"], pr["outer"], t, f, d, hf_focus=hf_f, hf_defocus=hf_d)) <= 2e-5, shape
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_tall_optimize_history_vs_oracle(model, shape):
+    f, d, F, D = model
+    t = strip_layout(shape, 7 + sum(shape))
+    r = b2.optimize(t, F, D, b2.OptConfig(max_iters=6, stop_patience=10**9, precision="fp32"))
+    ref = o.optimize(t, f, d, o.Cfg(max_iters=6, stop_patience=10**9))
+    h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag]
+                  for x in r.loss_history])
+    hr = np.array(ref.history)
+    assert h.shape == hr.shape == (6, 7)
+    assert np.allclose(h[:, :3], hr[:, :3], rtol=1e-4), (shape, h[:, :3], hr[:, :3])
+    # dt / max|v| are maxima over the whole grid (curvature-dominated pixels)
+    assert np.allclose(h[:, 3:5], hr[:, 3:5], rtol=1e-3), (shape, h[:, 3:5], hr[:, 3:5])

@@ -54,7 +54,7 @@ def test_strip_geometry():
         tiled.strip_geometry(64, 128, 2, 0, 35)
 
 
-def _halo_worker(rank, world, port, q, W, K):
+def _halo_worker(rank, world, port, q, W, K, tags):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -62,16 +62,20 @@ def _halo_worker(rank, world, port, q, W, K):
         phi = torch.full((8, s.ww), -1.0, dtype=torch.float64)
         i0, i1 = s.interior
         phi[:, i0:i1] = torch.as_tensor(s.columns()[i0:i1], dtype=torch.float64)
-        tiled.exchange_halos(phi, s)
+        tiled.exchange_halos(phi, s, tags=tags)
         q.put((rank, phi.numpy(), s.columns(), s.interior, s.halo))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("tags", [True, False])
 @pytest.mark.parametrize("world", [2, 4])
-def test_halo_exchange_gloo(world):
+def test_halo_exchange_gloo(world, tags):
+    """tags=False: every message carries the same tag, so the two messages
+    between the ranks of a world-2 ring are matched by position only -- the
+    way NCCL matches them (it ignores P2P tags)."""
     W, K = 1024, 35
-    for rank, phi, cols, (i0, i1), h in _run(world, _halo_worker, W, K):
+    for rank, phi, cols, (i0, i1), h in _run(world, _halo_worker, W, K, tags):
         # interior and HALO columns on each side hold the global column index (wrapping)
         assert np.array_equal(phi[:, i0 - h:i1 + h], np.broadcast_to(cols[i0 - h:i1 + h], (8, i1 - i0 + 2 * h)))
 
