@@ -222,6 +222,15 @@ int lsopc_session_time_passes(lsopc_session* s, int reps, double* ms_out);
 int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* rects_host, size_t rects_cap,
                    size_t* count);
 
+/* The same greedy fracture of a DEVICE mask (uint8 [H][W], non-zero = lit)
+ * on the GPU: one thread-block cluster runs the whole greedy loop with the
+ * lit bounding box's column heights in distributed shared memory; boxes too
+ * large for it finish on the host algorithm above.  Rectangles (x, y, w, h)
+ * go to host memory (rects_host may be NULL: count only).  Synchronises
+ * `stream`. */
+int lsopc_fracture_dev(int H, int W, const uint8_t* mask_dev, int32_t* rects_host, size_t rects_cap,
+                       size_t* count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,7 @@ _SIGS = {
     "lsopc_session_destroy": (_I, [_P]),
     "lsopc_session_launches_per_iter": (_I, [_P]),
     "lsopc_fracture": (_I, [_I, _I, _P, _P, _Z, ctypes.POINTER(_Z)]),
+    "lsopc_fracture_dev": (_I, [_I, _I, _P, _P, _Z, ctypes.POINTER(_Z), _P]),
     "lsopc_session_time_passes": (_I, [_P, _I, ctypes.POINTER(_D)]),
     "lsopc_session_set_tile": (_I, [_P, _I, _I, _I, _I]),
     "lsopc_dsn_init": (_I, [_Z, _P, _P, _D, _D, _D, _P, _P, _P]),
@@ -142,6 +143,21 @@ def torch():
 
 def stream():
     return _P(torch().cuda.current_stream().cuda_stream)
+
+
+_side = {}
+
+
+def side_stream():
+    """A second CUDA stream per (device, lane) for work that overlaps the
+    lane's main stream (the final shot count overlaps the result copies)."""
+    t = torch()
+    key = (t.cuda.current_device(), lane())
+    s = _side.get(key)
+    if s is None:
+        s = t.cuda.Stream()
+        _side[key] = s
+    return _P(s.cuda_stream)
 
 
 def ptr(t):

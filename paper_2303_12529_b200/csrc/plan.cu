@@ -69,6 +69,9 @@ struct DevBuf {
 
 }  // namespace
 
+// error text for lsopc_last_error() from the other translation units
+void lsb_set_error(const std::string& m) { g_err = m; }
+
 struct lsopc_plan {
   Grid g{};
   // idle sessions kept for reuse by the next lsopc_session_create with the

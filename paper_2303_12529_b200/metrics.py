@@ -1,7 +1,8 @@
 """Mask metrics: drop-in for the reference `lsopc.metrics` (metrics.py:1-108).
 
-L2 / PVBand are device popcounts; the greedy fracturing shot count is native
-host code in the same library (lsopc_fracture).
+L2 / PVBand are device popcounts; the greedy fracturing shot count runs on
+the GPU for device masks (lsopc_fracture_dev: one thread-block cluster) and
+as native host code for host masks (lsopc_fracture).
 """
 
 from __future__ import annotations
@@ -49,9 +50,46 @@ def pvband(z_in, z_out, pitch=1):
     return _count_neq(z_in, z_out) * pitch * pitch
 
 
+def _is_device(mask):
+    return hasattr(mask, "is_cuda") and mask.is_cuda
+
+
+def _device_u8(mask):
+    t = nv.torch()
+    if mask.dim() != 2:
+        raise ValueError("mask must be 2-D")
+    if mask.dtype != t.uint8:
+        mask = (mask != 0).to(t.uint8)
+    return mask.contiguous()
+
+
+def _fracture_dev(mask, rects=True, stream=None):
+    """Greedy fracture of a device mask on the GPU (lsopc_fracture_dev):
+    (count, [(x, y, w, h), ...] or None)."""
+    m = _device_u8(mask)
+    H, W = m.shape
+    sp = stream if stream is not None else nv.stream()
+    count = ctypes.c_size_t()
+    L = nv.lib()
+    if not rects:
+        nv.check(L.lsopc_fracture_dev(H, W, nv.ptr(m), None, 0, ctypes.byref(count), sp))
+        return int(count.value), None
+    cap = 1 << 16
+    while True:
+        buf = np.empty((cap, 4), dtype=np.int32)
+        nv.check(L.lsopc_fracture_dev(H, W, nv.ptr(m), buf.ctypes.data_as(ctypes.c_void_p), cap,
+                                      ctypes.byref(count), sp))
+        if count.value <= cap:
+            return int(count.value), [tuple(int(v) for v in r) for r in buf[:count.value]]
+        cap = int(count.value)
+
+
 def fracture(mask):
     """Greedy largest-rectangle decomposition, ties topmost then leftmost
-    (metrics.py:55-104).  Returns [(x, y, w, h), ...]."""
+    (metrics.py:55-104).  Returns [(x, y, w, h), ...].  A device (CUDA
+    tensor) mask is fractured on the GPU."""
+    if _is_device(mask):
+        return _fracture_dev(mask)[1]
     m = _as_u8(mask)
     if m.ndim != 2:
         raise ValueError("mask must be 2-D")
@@ -80,6 +118,9 @@ def _as_u8(mask):
 
 
 def shot_count(mask):
+    """len(fracture(mask)) (metrics.py:107-108); on the GPU for a device mask."""
+    if _is_device(mask):
+        return _fracture_dev(mask, rects=False)[0]
     m = _as_u8(mask)
     if m.ndim != 2:
         raise ValueError("mask must be 2-D")

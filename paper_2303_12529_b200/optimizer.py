@@ -341,10 +341,11 @@ def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, mod
                                      nv.stream()))
     # device -> host through a pinned staging buffer; wall_time is taken before
     # the shot count, as in the reference (optimizer.py:274-281).  The shot
-    # count (native, releases the GIL) of the final mask runs on a helper
-    # thread while the float64 phi is copied out.
+    # count of the final mask runs on the GPU (one thread-block cluster, on a
+    # side stream driven by a helper thread; the ctypes call releases the GIL)
+    # while the mask and the float64 phi are copied out.
+    shots = _tail_pool().submit(_device_shots, fmask, nv.side_stream())
     final_mask = nv.to_host(fmask)
-    shots = _tail_pool().submit(shot_count, final_mask)
     stage = nv.pinned_like(best)
     stage.copy_(best, non_blocking=True)
     nv.torch().cuda.current_stream().synchronize()
@@ -355,6 +356,11 @@ def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, mod
 
 
 _TAIL = None
+
+
+def _device_shots(fmask, stream):
+    from .metrics import _fracture_dev
+    return _fracture_dev(fmask, rects=False, stream=stream)[0]
 
 
 def _touched_empty(shape):
