@@ -50,12 +50,13 @@ LS_D void release_ticket(unsigned* ticket) {
   if (threadIdx.x == 0) *ticket = 0;
 }
 
-// optimizer.py:238-251: loss, best iterate, patience
+// optimizer.py:238-251: loss, best iterate, patience.  part: 4 partials per
+// block (losses, then the hard-print L2 / PVB counts of the same forward)
 LS_D void after_forward_body(const double* part, int nb, const LoopCfg& c, DevState* st, double* hist,
                              double* red) {
   if (st->stopped) return;
-  double l[2];
-  reduce_partials<2, false>(part, nb, l, red);
+  double l[4];  // L_ilt, L_pvb, hard-print L2 count, hard-print PVB count
+  reduce_partials<4, false>(part, nb, l, red);
   if (threadIdx.x != 0) return;
   const double l_ilt = l[0], l_pvb = l[1];
   const double l_dso = c.alpha * l_ilt + c.beta * l_pvb;
@@ -73,6 +74,9 @@ LS_D void after_forward_body(const double* part, int nb, const LoopCfg& c, DevSt
     rel = isfinite(st->best) ? (st->best - l_dso) / st->best : CUDART_INF;
     st->best = l_dso;
     st->improved = 1;
+    st->best_l2 = l[2];
+    st->best_pvb = l[3];
+    st->have_counts = 1;
   } else {
     rel = 0.0;
   }

@@ -87,7 +87,8 @@ int reduce_blocks();   // number of partial slots used by grid-stride reducers
 struct ResistParams {
   double i_th, sigma_z, alpha, beta;
 };
-// Z corners from intensities (R), losses into partials[blk*2+{0,1}], gates wf/wd
+// Z corners from intensities (R), partials[blk*4+{0..3}] = L_ilt, L_pvb and the
+// hard-print L2 / PVB counts (with a target), gates wf/wd
 // (R, nullable), Z outputs (f64, nullable), hard prints (u8, nullable).
 void launch_resist(const Grid& g, const void* If, const void* Id, const uint8_t* target_u8,
                    const double* target_f64, ResistParams p, void* wf, void* wd,

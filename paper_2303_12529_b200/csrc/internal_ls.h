@@ -15,6 +15,11 @@ struct DevState {
   double vmax, gmax, dt;
   int stopped, improved, use_beta, streak, nhist, nonfinite_it;
   int it;  // index of the iteration in flight (advanced by the update's control kernel)
+  // hard-print L2 / PVBand counts (metrics.py:39-52) of the best iterate,
+  // recorded by the forward that found it: the result's metrics without a
+  // final forward pass (optimizer.py:271-277 recomputes the same prints)
+  double best_l2, best_pvb;
+  int have_counts;
   unsigned ticket[4];  // last-block tickets of the fused control tails (control.cuh), zero between launches
 };
 
@@ -74,6 +79,9 @@ void launch_elementwise(int op, size_t n, const double* a, const double* b, doub
 // out: device scalar.  W > 0 restricts RD_COUNTNEQ8 to columns [ix0, ix1) of rows of width W.
 void launch_reduce(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
                    double* partials, double* out, cudaStream_t s, int W = 0, int ix0 = 0, int ix1 = 0);
+
+// p[i] = p[i] != 0 (uint8, in place; 16-byte aligned p)
+void launch_binarize_u8(size_t n, uint8_t* p, cudaStream_t s);
 
 // exact EDT -> truncated signed distance (levelset.py:86-101)
 void launch_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_lower, double* phi,

@@ -309,7 +309,7 @@ __global__ void k_copy_best(size_t n, const double* __restrict__ phi, double* be
 // runs the same bodies as fused tails of their producers (control.cuh)
 
 __global__ void k_after_forward(const double* part, int nb, LoopCfg c, DevState* st, double* hist) {
-  __shared__ double red[64];
+  __shared__ double red[128];
   after_forward_body(part, nb, c, st, hist, red);
 }
 __global__ void k_after_grad(const double* dots, int nb, int restart_every, DevState* st) {
@@ -348,6 +348,26 @@ __global__ void k_elementwise(int op, size_t n, const double* __restrict__ a, co
       default: break;
     }
   }
+}
+
+// target != 0 -> 0 / 1 bytes in place (optimizer.py:197: np.asarray(target) != 0),
+// 16 bytes per thread step
+__global__ void k_binarize_u8(size_t n, uint8_t* p) {
+  const size_t n16 = n / 16;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    uint4 v = reinterpret_cast<uint4*>(p)[i];
+    uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // per byte: 1 if non-zero
+      const uint32_t x = w[k];
+      const uint32_t nz = ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x;
+      w[k] = (nz >> 7) & 0x01010101u;
+    }
+    reinterpret_cast<uint4*>(p)[i] = v;
+  }
+  for (size_t i = n16 * 16 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = p[i] != 0;
 }
 
 // DevelSet-Net outputs -> DSO inputs in one pass (boundary
@@ -391,7 +411,7 @@ k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restric
 
 template <int NV, bool MAX>
 __global__ void k_reduce_partials(const double* part, int nb, double* out) {
-  __shared__ double red[64];
+  __shared__ double red[32 * NV];
   double r[NV];
   reduce_partials<NV, MAX>(part, nb, r, red);
   if (threadIdx.x == 0)
@@ -451,7 +471,9 @@ void launch_dsn_init(size_t n, const float* phi_raw, const float* m_raw, double 
   k_dsn_init<<<kBlocks, kThreads, 0, s>>>(n, phi_raw, m_raw, lo, hi, eps, phi0, m);
 }
 void launch_reduce_partials(const double* part, int nb, int nv, int is_max, double* out, cudaStream_t s) {
-  if (nv == 1) {
+  if (nv == 4) {
+    k_reduce_partials<4, false><<<1, 256, 0, s>>>(part, nb, out);
+  } else if (nv == 1) {
     if (is_max) k_reduce_partials<1, true><<<1, 256, 0, s>>>(part, nb, out);
     else k_reduce_partials<1, false><<<1, 256, 0, s>>>(part, nb, out);
   } else {
@@ -462,6 +484,9 @@ void launch_reduce_partials(const double* part, int nb, int nv, int is_max, doub
 void launch_elementwise(int op, size_t n, const double* a, const double* b, double p0, double p1, double p2,
                         double* out, uint8_t* out8, cudaStream_t s) {
   k_elementwise<<<kBlocks, kThreads, 0, s>>>(op, n, a, b, p0, p1, p2, out, out8);
+}
+void launch_binarize_u8(size_t n, uint8_t* p, cudaStream_t s) {
+  k_binarize_u8<<<kBlocks, kThreads, 0, s>>>(n, p);
 }
 void launch_reduce(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
                    double* partials, double* out, cudaStream_t s, int W, int ix0, int ix1) {

@@ -218,7 +218,7 @@ int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
       p->Id.ensure(n * p->g.rsize());
       p->wf.ensure(n * p->g.rsize());
       p->wd.ensure(n * p->g.rsize());
-      size_t np = (size_t)std::max(std::max(reduce_blocks(), ls_blocks()), H) * 2 + 64;
+      size_t np = (size_t)std::max(std::max(reduce_blocks(), ls_blocks()), H) * 4 + 64;
       p->partials.ensure(np * sizeof(double));
       p->scal.ensure(64 * sizeof(double));
       p->hard.ensure(3 * n);
@@ -597,7 +597,7 @@ void enqueue_phase(lsopc_session* ss, int phase, cudaStream_t s) {
       ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
       launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr,
                     nullptr, nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s, t.ix0, t.ix1);
-      launch_reduce_partials(p->partials.as<double>(), reduce_blocks(), 2, 0, sc, s);
+      launch_reduce_partials(p->partials.as<double>(), reduce_blocks(), 4, 0, sc, s);
     } break;
     case 1: {  // stop rule on the global losses; adjoint -> sum PR dots
       LoopCfg lc{c.alpha, c.beta, c.stop_rel_tol, c.stop_patience};
@@ -706,6 +706,7 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
         if (mod_dev) ss->mod.ensure(n * 8);
       }
       ck(cudaMemcpyAsync(ss->target.p, target_dev, n, cudaMemcpyDeviceToDevice, s), "memcpy");
+      launch_binarize_u8(n, ss->target.as<uint8_t>(), s);  // any non-zero byte is lit (optimizer.py:197)
       // optimizer.py:197-201: uniform target -> DegenerateInputError
       if (!cfg->skip_target_check) {
         double lit = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, ss->target.as<uint8_t>(), nullptr, plan, s);
@@ -782,21 +783,31 @@ int lsopc_session_finish(lsopc_session* ss, double* best_phi_dev, uint8_t* final
     if (history_host && h.nhist > 0)
       ck(cudaMemcpy(history_host, ss->hist.p, (size_t)h.nhist * 7 * sizeof(double), cudaMemcpyDeviceToHost),
          "memcpy");
-    // optimizer.py:271-277: best phi -> mask -> hard corners -> L2 / PVB
+    // optimizer.py:271-277: best phi -> mask -> hard corners -> L2 / PVB.  The
+    // forward that found the best iterate already counted its hard prints
+    // (same mask bytes, same kernels: bit-identical intensities), so a
+    // whole-grid session takes those counts; strips and sessions without an
+    // iteration run the final forward.
     uint8_t* fm = final_mask_dev ? final_mask_dev : ss->mask.as<uint8_t>();
     launch_elementwise(EW_MASK, n, ss->best.as<double>(), nullptr, 0, 0, 0, nullptr, fm, s);
-    launch_mask_fft(g, fm, nullptr, nullptr, p->mhat.p, p->scratch.p, nullptr, s);
-    forward(p, ss->focus, ss->defocus, nullptr, s);
-    uint8_t* hn = p->hard.as<uint8_t>();
-    ResistParams rp{ss->cfg.i_th, ss->cfg.sigma_z, 0.0, 0.0};
-    launch_resist(g, p->If.p, p->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr, nullptr, hn, hn + n,
-                  hn + 2 * n, nullptr, nullptr, s);
-    ck_launch("final prints");
-    const int cw = ss->tiled ? g.W : 0;  // strip: count the interior columns only
-    double l2 = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn, ss->target.as<uint8_t>(), p, s, cw,
-                               ss->tile.ix0, ss->tile.ix1);
-    double pvb = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn + n, hn + 2 * n, p, s, cw, ss->tile.ix0,
-                                ss->tile.ix1);
+    double l2, pvb;
+    if (!ss->tiled && h.have_counts) {
+      l2 = h.best_l2;
+      pvb = h.best_pvb;
+    } else {
+      launch_mask_fft(g, fm, nullptr, nullptr, p->mhat.p, p->scratch.p, nullptr, s);
+      forward(p, ss->focus, ss->defocus, nullptr, s);
+      uint8_t* hn = p->hard.as<uint8_t>();
+      ResistParams rp{ss->cfg.i_th, ss->cfg.sigma_z, 0.0, 0.0};
+      launch_resist(g, p->If.p, p->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr, nullptr, hn,
+                    hn + n, hn + 2 * n, nullptr, nullptr, s);
+      ck_launch("final prints");
+      const int cw = ss->tiled ? g.W : 0;  // strip: count the interior columns only
+      l2 = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn, ss->target.as<uint8_t>(), p, s, cw, ss->tile.ix0,
+                          ss->tile.ix1);
+      pvb = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn + n, hn + 2 * n, p, s, cw, ss->tile.ix0,
+                           ss->tile.ix1);
+    }
     if (best_phi_dev) ck(cudaMemcpyAsync(best_phi_dev, ss->best.p, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
     ck(cudaStreamSynchronize(s), "sync");
     if (res) {
@@ -832,7 +843,7 @@ int lsopc_session_losses(lsopc_session* ss, double* l_ilt, double* l_pvb, double
     double* sc = ss->scalars.as<double>();
     launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, nullptr, nullptr, nullptr, nullptr,
                   nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), nullptr, s);
-    launch_reduce_partials(p->partials.as<double>(), reduce_blocks(), 2, 0, sc, s);
+    launch_reduce_partials(p->partials.as<double>(), reduce_blocks(), 4, 0, sc, s);
     double h[2];
     ck(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, s), "memcpy");
     ck(cudaStreamSynchronize(s), "sync");

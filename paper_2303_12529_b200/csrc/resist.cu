@@ -29,9 +29,9 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
          const double* __restrict__ tf, ResistParams p, R* wf, R* wd, double* z_nom, double* z_in,
          double* z_out, uint8_t* h_nom, uint8_t* h_in, uint8_t* h_out, double* partials,
          StopFlag stop, int W, int ix0, int ix1) {
-  __shared__ double red[64];
+  __shared__ double red[128];
   if (stop && *stop) return;
-  double acc[2] = {0.0, 0.0};
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const bool have_t = tu8 || tf;
   const RowSplit rs = row_split(W);
   const bool whole = ix0 <= 0 && ix1 >= W;
@@ -62,6 +62,9 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
       if (x >= ix0 && x < ix1) {         // strip interior (the whole row by default)
         acc[0] += dn * dn;               // optimizer.py:88-90
         acc[1] += di * di + dout * dout;  // optimizer.py:93-96
+        // hard prints (litho.py:129-131): L2 vs the target, PVB inner vs outer (metrics.py:39-52)
+        acc[2] += ((i_nom >= p.i_th) != (zt != 0.0)) ? 1.0 : 0.0;
+        acc[3] += ((i_in >= p.i_th) != (i_out >= p.i_th)) ? 1.0 : 0.0;
       }
       if (wf) {
         // optimizer.py:109 gate, 114-134 doses and alpha/beta folded per kernel set
@@ -74,11 +77,9 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
     }
   }
   if (partials) {
-    block_sum<2>(acc, red);
-    if (threadIdx.x == 0) {
-      partials[2 * blockIdx.x] = acc[0];
-      partials[2 * blockIdx.x + 1] = acc[1];
-    }
+    block_sum<4>(acc, red);
+    if (threadIdx.x == 0)
+      for (int j = 0; j < 4; ++j) partials[4 * blockIdx.x + j] = acc[j];
   }
 }
 
@@ -107,9 +108,9 @@ __global__ void __launch_bounds__(kRedThreads)
 k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, const uint8_t* __restrict__ tu8,
               const double* __restrict__ tf, ResistParams p, R* wf, R* wd, double* partials, StopFlag stop, int W,
               int ix0, int ix1, LoopTail tail) {
-  __shared__ double red[64];
+  __shared__ double red[128];
   if (stop && *stop) return;
-  double acc[2] = {0.0, 0.0};
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const RowSplit rs = row_split(W);
   const bool whole = ix0 <= 0 && ix1 >= W;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n4; g += (size_t)gridDim.x * blockDim.x) {
@@ -141,6 +142,8 @@ k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, con
       if (whole || (x0 + e >= ix0 && x0 + e < ix1)) {
         acc[0] += dn * dn;
         acc[1] += di * di + dout * dout;
+        acc[2] += ((i_nom >= p.i_th) != (zt[e] != 0.0)) ? 1.0 : 0.0;
+        acc[3] += ((i_in >= p.i_th) != (i_out >= p.i_th)) ? 1.0 : 0.0;
       }
       gf[e] = (R)(p.alpha * (dn * zn * (1.0 - zn)) + p.beta * 1.02 * (dout * zo * (1.0 - zo)));
       gd[e] = (R)(p.beta * 0.98 * (di * zi * (1.0 - zi)));
@@ -150,11 +153,9 @@ k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, con
       st4(wd, i, gd);
     }
   }
-  block_sum<2>(acc, red);
-  if (threadIdx.x == 0) {
-    partials[2 * blockIdx.x] = acc[0];
-    partials[2 * blockIdx.x + 1] = acc[1];
-  }
+  block_sum<4>(acc, red);
+  if (threadIdx.x == 0)
+    for (int j = 0; j < 4; ++j) partials[4 * blockIdx.x + j] = acc[j];
   if (tail.st && last_block(&tail.st->ticket[0], red)) {
     after_forward_body(partials, gridDim.x, tail.c, tail.st, tail.hist, red);
     release_ticket(&tail.st->ticket[0]);

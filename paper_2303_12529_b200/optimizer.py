@@ -255,8 +255,24 @@ def _check_kernel_sets(shape, focus_kernels, defocus_kernels):
                              f"process condition {sel!r}")
 
 
-def _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation):
-    target = _check_target(target)
+def _target_bytes(target):
+    """The target as contiguous uint8 bytes without a host pass when it
+    already is uint8 / bool (the device binarises it); other dtypes are
+    binarised here."""
+    t = np.asarray(target)
+    if t.ndim != 2:
+        raise ValueError("target must be a 2-D layout")
+    if t.dtype == np.bool_:
+        t = t.view(np.uint8)
+    elif t.dtype != np.uint8:
+        t = np.not_equal(t, 0).view(np.uint8)
+    return np.ascontiguousarray(t)
+
+
+def _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation, scan=True):
+    """Validation of optimize's inputs (optimizer.py:197-228).  scan=False
+    leaves the uniform-target check to the device (lsopc_session_create)."""
+    target = _check_target(target) if scan else _target_bytes(target)
     shape = target.shape
     if phi0 is not None and phi0.shape != shape:
         raise ValueError("phi0 dimensions do not match target")
@@ -322,37 +338,37 @@ def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, mod
     if _is_device_tensor(phi0) or _is_device_tensor(modulation):
         target, fk, dk, p0, mdv = _device_inputs(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
     else:
-        target, m, fk, dk = _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
+        target, m, fk, dk = _prepare(target, focus_kernels, defocus_kernels, cfg, phi0, modulation, scan=False)
         p0 = nv.to_dev(phi0.phi) if phi0 is not None else None
         mdv = nv.to_dev(m) if m is not None else None
     shape = target.shape
+    # the raw bytes go up; the device binarises them (target != 0) and
+    # rejects a uniform target (optimizer.py:197-201) in lsopc_session_create
     td = nv.to_dev_staged(target, np.uint8)
     best = nv.empty(shape, np.float64)
     fmask = nv.empty(shape, np.uint8)
     hist = np.zeros((cfg.max_iters + 1, 7))
     res = nv.LsopcResult()
     c = _native_cfg(cfg)
-    # the host array for the float64 phi is allocated and faulted in on a
-    # helper thread while the loop runs (the ctypes call releases the GIL)
-    phi_host = _tail_pool().submit(_touched_empty, shape)
     nv.check(nv.lib().lsopc_optimize(fk.plan.handle, fk.handle, dk.handle, nv.ptr(td), nv.ptr(p0),
                                      nv.ptr(mdv), ctypes.byref(c), nv.ptr(best), nv.ptr(fmask),
                                      hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res),
                                      nv.stream()))
-    # device -> host through a pinned staging buffer; wall_time is taken before
-    # the shot count, as in the reference (optimizer.py:274-281).  The shot
-    # count of the final mask runs on the GPU (one thread-block cluster, on a
-    # side stream driven by a helper thread; the ctypes call releases the GIL)
-    # while the mask and the float64 phi are copied out.
+    # wall_time is taken before the shot count, as in the reference
+    # (optimizer.py:274-281).  The shot count of the final mask runs on the GPU
+    # (one thread-block cluster, on a side stream driven by a helper thread;
+    # the ctypes call releases the GIL) while the mask and the float64 phi are
+    # copied straight into page-locked host tensors from torch's caching host
+    # allocator, whose numpy views are the returned arrays (no host-side copy).
     shots = _tail_pool().submit(_device_shots, fmask, nv.side_stream())
-    final_mask = nv.to_host(fmask)
-    stage = nv.pinned_like(best)
-    stage.copy_(best, non_blocking=True)
-    nv.torch().cuda.current_stream().synchronize()
-    best_phi = phi_host.result()
-    np.copyto(best_phi, stage.numpy())
+    t = nv.torch()
+    mask_h = t.empty(shape, dtype=t.uint8, pin_memory=True)
+    phi_h = t.empty(shape, dtype=t.float64, pin_memory=True)
+    mask_h.copy_(fmask, non_blocking=True)
+    phi_h.copy_(best, non_blocking=True)
+    t.cuda.current_stream().synchronize()
     wall = time.perf_counter() - t0
-    return final_mask, best_phi, (res.iters, res.l2, res.pvband), hist, wall, shots
+    return mask_h.numpy(), phi_h.numpy(), (res.iters, res.l2, res.pvband), hist, wall, shots
 
 
 _TAIL = None
@@ -361,12 +377,6 @@ _TAIL = None
 def _device_shots(fmask, stream):
     from .metrics import _fracture_dev
     return _fracture_dev(fmask, rects=False, stream=stream)[0]
-
-
-def _touched_empty(shape):
-    a = np.empty(shape, dtype=np.float64)
-    a.fill(0.0)  # fault the pages in now, off the critical path
-    return a
 
 
 def _tail_pool():

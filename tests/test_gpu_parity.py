@@ -616,3 +616,19 @@ def test_device_initial_state_validates_like_host():
     assert np.array_equal(_hist(r_host), _hist(r_mix))
     with pytest.raises(ValueError):
         b2.optimize(t, F, D, b2.OptConfig(max_iters=2), phi0=dev_phi, modulation=np.full(t.shape, 2.0))
+
+
+def test_optimize_target_dtypes_binarised():
+    """optimize binarises the target as `np.asarray(target) != 0`
+    (optimizer.py:197): uint8 values other than 1, bool and int layouts give
+    the 0/1 result; uniform targets still raise."""
+    nv.set_precision("fp64")
+    f, d, F, D = kernels(9, 2, 0)
+    t = o.rect_layout(64, [(10, 12, 20, 30), (40, 8, 12, 12)])
+    ref = b2.optimize(t, F, D, b2.OptConfig(max_iters=4))
+    for alt in (t * 7, t.astype(bool), t.astype(np.int32) * -3):
+        r = b2.optimize(alt, F, D, b2.OptConfig(max_iters=4))
+        assert np.array_equal(_hist(r), _hist(ref)) and np.array_equal(r.final_mask, ref.final_mask)
+        assert (r.metrics.l2, r.metrics.pvband) == (ref.metrics.l2, ref.metrics.pvband)
+    with pytest.raises(b2.DegenerateInputError):
+        b2.optimize(np.full((32, 32), 5, dtype=np.uint8), F, D, b2.OptConfig(max_iters=2))
