@@ -138,6 +138,13 @@ typedef struct {
   /* 1: skip the uniform-target check (a strip of a larger tile may be uniform;
    * the caller checks the whole tile, optimizer.py:197-201) */
   int skip_target_check;
+  /* Opt-in extensions (not in the reference; 0 = the reference's behaviour):
+   * grad_scheme 1: Godunov upwind |grad phi| in the update term instead of the
+   * central one (levelset.py:60-62); reinit_every N > 0: after every N-th
+   * completed iteration phi <- TSDF(mask_from_phi(phi)) (levelset.py:86-101),
+   * whole-grid sessions only. */
+  int grad_scheme;
+  int reinit_every;
 } lsopc_config;
 
 typedef struct {
@@ -221,6 +228,17 @@ int lsopc_session_time_passes(lsopc_session* s, int reps, double* ms_out);
  * returns the count via *count. */
 int lsopc_fracture(int H, int W, const uint8_t* mask_host, int32_t* rects_host, size_t rects_cap,
                    size_t* count);
+
+/* EXTENSION (no reference implementation; parity UNPINNED):
+ * edge placement error of a printed image against its target, both uint8
+ * DEVICE grids [H][W] (non-zero = lit).  Samples on the target's edges at a
+ * lattice (horizontal edges at columns x = offset mod spacing, vertical edges
+ * at rows y = offset mod spacing); EPE = signed displacement of the printed
+ * edge along the outward normal, saturating at max_search; a violation when
+ * |EPE| > threshold.  out_host[4] = samples, violations, sum |EPE|,
+ * max |EPE|.  Synchronises `stream`. */
+int lsopc_epe(int H, int W, const uint8_t* print_dev, const uint8_t* target_dev, int spacing, int offset,
+              int threshold, int max_search, double* out_host, void* stream);
 
 /* The same greedy fracture of a DEVICE mask (uint8 [H][W], non-zero = lit)
  * on the GPU: one thread-block cluster runs the whole greedy loop with the

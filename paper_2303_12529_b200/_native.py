@@ -36,7 +36,8 @@ class LsopcConfig(ctypes.Structure):
                 ("max_iters", ctypes.c_int), ("stop_rel_tol", ctypes.c_double),
                 ("stop_patience", ctypes.c_int), ("use_curvature", ctypes.c_int),
                 ("cg_restart_every", ctypes.c_int), ("update_form", ctypes.c_int),
-                ("skip_target_check", ctypes.c_int)]
+                ("skip_target_check", ctypes.c_int), ("grad_scheme", ctypes.c_int),
+                ("reinit_every", ctypes.c_int)]
 
 
 class LsopcResult(ctypes.Structure):
@@ -79,6 +80,7 @@ _SIGS = {
     "lsopc_session_launches_per_iter": (_I, [_P]),
     "lsopc_fracture": (_I, [_I, _I, _P, _P, _Z, ctypes.POINTER(_Z)]),
     "lsopc_fracture_dev": (_I, [_I, _I, _P, _P, _Z, ctypes.POINTER(_Z), _P]),
+    "lsopc_epe": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, ctypes.POINTER(_D), _P]),
     "lsopc_session_time_passes": (_I, [_P, _I, ctypes.POINTER(_D)]),
     "lsopc_session_set_tile": (_I, [_P, _I, _I, _I, _I]),
     "lsopc_dsn_init": (_I, [_Z, _P, _P, _D, _D, _D, _P, _P, _P]),

@@ -60,7 +60,8 @@ void launch_curvature(int H, int W, const double* phi, const double* m, double w
 // (after_update) in the kernel's last block instead of a separate launch
 void launch_ls_velocity(int H, int W, const double* phi, const double* v, const double* dprev, const double* m,
                         double weight, int use_curv, DevState* st, double* d, double* u, double* gm,
-                        double* partials, Tile t, cudaStream_t s, const LoopTail* tail = nullptr);
+                        double* partials, Tile t, cudaStream_t s, const LoopTail* tail = nullptr,
+                        int upwind = 0);
 void launch_ls_update(int H, int W, double* phi, const double* u, const double* gm, double lo, double hi,
                       DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s,
                       const LoopTail* tail = nullptr);
@@ -84,8 +85,14 @@ void launch_reduce(int op, size_t n, const double* a, const double* b, const uin
 void launch_binarize_u8(size_t n, uint8_t* p, cudaStream_t s);
 
 // exact EDT -> truncated signed distance (levelset.py:86-101)
+// skip (nullable, device): every kernel returns at entry when *skip != 0
 void launch_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_lower, double* phi,
-                 int* scratch_i32, double* scratch_f64, cudaStream_t s);
+                 int* scratch_i32, double* scratch_f64, cudaStream_t s, const int* skip = nullptr);
+// Opt-in periodic reinitialisation of the DSO loop (extension): after the
+// update of iteration it, *skip = 0 iff the loop runs, (it + 1) % every == 0
+// and the mask (lit count *lit of n) is not uniform; phi is then replaced by
+// the exact TSDF of its own mask.
+void launch_reinit_gate(const DevState* st, const double* lit, double n, int every, int* skip, cudaStream_t s);
 size_t tsdf_scratch_i32(int H, int W);
 size_t tsdf_scratch_f64(int H, int W);
 

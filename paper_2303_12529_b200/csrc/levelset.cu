@@ -124,16 +124,45 @@ k_curvature(int H, int W, const double* __restrict__ phi, const double* __restri
 
 // ---- loop kernels -------------------------------------------------------------
 
-// Stencil input of one pixel (levelset.py:112-118 operands + the loop fields)
+// Stencil input of one pixel (levelset.py:112-118 operands + the loop fields);
+// dmx .. dpy: one-sided differences for the opt-in upwind |grad phi|
 struct VelIn {
   Geom g;
   double v, dp, m;
+  double dmx, dpx, dmy, dpy;
 };
+
+// Opt-in extension (not in the reference, which uses the central |grad phi|
+// of levelset.py:60-62 in the update): Godunov upwind |grad phi| for
+// phi_t + F |grad phi| = 0 with F = v_total (Osher & Sethian), one-sided
+// differences with replicate padding, summed in the order
+// max(D-x,0)^2 + min(D+x,0)^2 + max(D-y,0)^2 + min(D+y,0)^2 for F > 0 and the
+// mirrored terms otherwise (oracle/lsopc_oracle.py grad_mag_upwind).
+LS_D double upwind_mag(const VelIn& a, double F) {
+  double tx0, tx1, ty0, ty1;
+  if (F > 0.0) {
+    tx0 = fmax(a.dmx, 0.0); tx1 = fmin(a.dpx, 0.0); ty0 = fmax(a.dmy, 0.0); ty1 = fmin(a.dpy, 0.0);
+  } else {
+    tx0 = fmin(a.dmx, 0.0); tx1 = fmax(a.dpx, 0.0); ty0 = fmin(a.dmy, 0.0); ty1 = fmax(a.dpy, 0.0);
+  }
+  return __dsqrt_rn(add(add(add(mul(tx0, tx0), mul(tx1, tx1)), mul(ty0, ty0)), mul(ty1, ty1)));
+}
+
+// one-sided differences at (y, x) with the stencil's clamps (slow path)
+LS_D void one_sided_at(const double* __restrict__ phi, int H, int W, int y, int x, int xlo, int xhi, VelIn& a) {
+  const int xe = x + 1 < xhi ? x + 1 : xhi - 1, xw = x > xlo ? x - 1 : xlo;
+  const int ys = y + 1 < H ? y + 1 : H - 1, yn = y > 0 ? y - 1 : 0;
+  const double c = phi[(size_t)y * W + x];
+  a.dmx = sub(c, phi[(size_t)y * W + xw]);
+  a.dpx = sub(phi[(size_t)y * W + xe], c);
+  a.dmy = sub(c, phi[(size_t)yn * W + x]);
+  a.dpy = sub(phi[(size_t)ys * W + x], c);
+}
 
 // _step_fields (optimizer.py:180-194) + the update field of optimizer.py:262:
 //   d = -v (+ beta d_prev); v_total = d - kappa/(|grad phi| + 1e-8); u = -v_total |grad phi|
 LS_D double vel_emit(const VelIn& a, int use_beta, double beta, int use_curv, bool have_m, double weight,
-                     double& gm_out, double& d_out) {
+                     double& gm_out, double& d_out, double& gu_out, int upwind) {
   const double gm = np_hypot(a.g.gx, a.g.gy);
   double d = -a.v;
   if (use_beta) d = add(d, mul(beta, a.dp));
@@ -145,6 +174,7 @@ LS_D double vel_emit(const VelIn& a, int use_beta, double beta, int use_curv, bo
   }
   gm_out = gm;
   d_out = d;
+  gu_out = upwind ? upwind_mag(a, vt) : gm;  // |grad phi| of the update term
   return vt;
 }
 
@@ -153,11 +183,13 @@ LS_D double vel_emit(const VelIn& a, int use_beta, double beta, int use_curv, bo
 // fields as double2, so each thread keeps enough bytes in flight; pairs that
 // touch a clamped column fall back to the per-pixel stencil.
 constexpr int kVelThreads = 192;  // 80 registers: four 6-warp blocks per SM keep kBlocks one wave
+template <bool UPWIND>
 __global__ void __launch_bounds__(kVelThreads, kBlocks / 148)
 k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __restrict__ v,
               const double* __restrict__ dprev, const double* __restrict__ m, double weight, int use_curv,
               DevState* st, double* d_out, double* u_out, double* gm_out, double* partials, Tile tl,
               LoopTail tail) {
+  constexpr int upwind = UPWIND;
   __shared__ double red[64];
   if (st->stopped) return;
   const int use_beta = st->use_beta;
@@ -188,10 +220,20 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
         g.gxx = sub(add(ee, w), mul(2.0, c));
         g.gyy = sub(add(s, nn), mul(2.0, c));
         g.gxy = mul(0.25, sub(sub(S0[2 + e], S0[e]), sub(N0[2 + e], N0[e])));
+        if (upwind) {
+          a[e].dmx = sub(c, w);
+          a[e].dpx = sub(ee, c);
+          a[e].dmy = sub(c, nn);
+          a[e].dpy = sub(s, c);
+        }
       }
     } else {
       a[0].g = geometry_at(phi, H, W, y, x, tl.xlo, tl.xhi);
       a[1].g = geometry_at(phi, H, W, y, x + 1, tl.xlo, tl.xhi);
+      if (upwind) {
+        one_sided_at(phi, H, W, y, x, tl.xlo, tl.xhi, a[0]);
+        one_sided_at(phi, H, W, y, x + 1, tl.xlo, tl.xhi, a[1]);
+      }
     }
     const double2 vv = *reinterpret_cast<const double2*>(v + i);
     a[0].v = vv.x;
@@ -210,15 +252,16 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
     } else {
       a[0].m = a[1].m = 1.0;
     }
-    double vt[2], gm[2], d[2];
+    double vt[2], gm[2], d[2], gu[2];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) vt[e] = vel_emit(a[e], use_beta, beta, use_curv, m != nullptr, weight, gm[e], d[e]);
+    for (int e = 0; e < 2; ++e)
+      vt[e] = vel_emit(a[e], use_beta, beta, use_curv, m != nullptr, weight, gm[e], d[e], gu[e], upwind);
     *reinterpret_cast<double2*>(d_out + i) = make_double2(d[0], d[1]);
     if (gm_out) {  // modulation_search form: keep v_total and |grad phi| apart
       *reinterpret_cast<double2*>(u_out + i) = make_double2(vt[0], vt[1]);
-      *reinterpret_cast<double2*>(gm_out + i) = make_double2(gm[0], gm[1]);
+      *reinterpret_cast<double2*>(gm_out + i) = make_double2(gu[0], gu[1]);
     } else {
-      *reinterpret_cast<double2*>(u_out + i) = make_double2(mul(-vt[0], gm[0]), mul(-vt[1], gm[1]));
+      *reinterpret_cast<double2*>(u_out + i) = make_double2(mul(-vt[0], gu[0]), mul(-vt[1], gu[1]));
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -323,6 +366,12 @@ __global__ void k_after_velocity(const double* part, int nb, double eta, DevStat
 __global__ void k_after_update(const double* part, int nb, DevState* st, double* hist) {
   __shared__ double red[32];
   after_update_body(part, nb, st, hist, red);
+}
+
+// opt-in reinitialisation gate (internal_ls.h launch_reinit_gate)
+__global__ void k_reinit_gate(const DevState* st, const double* lit, double n, int every, int* skip) {
+  const double c = *lit;
+  *skip = (st->stopped || every <= 0 || st->it % every != 0 || c == 0.0 || c == n) ? 1 : 0;
 }
 
 // ---- elementwise API operators -------------------------------------------------
@@ -440,10 +489,14 @@ void launch_curvature(int H, int W, const double* phi, const double* m, double w
 }
 void launch_ls_velocity(int H, int W, const double* phi, const double* v, const double* dprev, const double* m,
                         double weight, int use_curv, DevState* st, double* d, double* u, double* gm,
-                        double* partials, Tile t, cudaStream_t s, const LoopTail* tail) {
+                        double* partials, Tile t, cudaStream_t s, const LoopTail* tail, int upwind) {
   if (W % 4) throw std::invalid_argument("level-set loop kernels need a width divisible by 4");
-  k_ls_velocity<<<kBlocks, kVelThreads, 0, s>>>(H, W, phi, v, dprev, m, weight, use_curv, st, d, u, gm, partials, t,
-                                                tail ? *tail : LoopTail{});
+  if (upwind)
+    k_ls_velocity<true><<<kBlocks, kVelThreads, 0, s>>>(H, W, phi, v, dprev, m, weight, use_curv, st, d, u, gm,
+                                                        partials, t, tail ? *tail : LoopTail{});
+  else
+    k_ls_velocity<false><<<kBlocks, kVelThreads, 0, s>>>(H, W, phi, v, dprev, m, weight, use_curv, st, d, u, gm,
+                                                         partials, t, tail ? *tail : LoopTail{});
 }
 void launch_ls_update(int H, int W, double* phi, const double* u, const double* gm, double lo, double hi,
                       DevState* st, uint8_t* mask, double* partials, Tile t, cudaStream_t s, const LoopTail* tail) {
@@ -484,6 +537,9 @@ void launch_reduce_partials(const double* part, int nb, int nv, int is_max, doub
 void launch_elementwise(int op, size_t n, const double* a, const double* b, double p0, double p1, double p2,
                         double* out, uint8_t* out8, cudaStream_t s) {
   k_elementwise<<<kBlocks, kThreads, 0, s>>>(op, n, a, b, p0, p1, p2, out, out8);
+}
+void launch_reinit_gate(const DevState* st, const double* lit, double n, int every, int* skip, cudaStream_t s) {
+  k_reinit_gate<<<1, 1, 0, s>>>(st, lit, n, every, skip);
 }
 void launch_binarize_u8(size_t n, uint8_t* p, cudaStream_t s) {
   k_binarize_u8<<<kBlocks, kThreads, 0, s>>>(n, p);

@@ -433,6 +433,7 @@ struct lsopc_session {
   lsopc_config cfg{};
   cudaStream_t s = nullptr;
   DevBuf target, phi, best, v[2], d[2], u, mask, mod, hist, state, part_ls, part_up, dots, gm;
+  DevBuf rein;  // opt-in reinitialisation: reduce partials, lit count, gate flag
   int it = 0;  // iterations enqueued
   bool have_mod = false;
   // strip of an oversized tile (lsopc_session_set_tile): interior / stencil columns
@@ -456,7 +457,7 @@ struct lsopc_session {
       if (e) cudaEventDestroy(e);
     if (hflag) cudaFreeHost(hflag);
     for (DevBuf* b : {&target, &phi, &best, &v[0], &v[1], &d[0], &d[1], &u, &mask, &mod, &hist, &state, &part_ls,
-                      &part_up, &dots, &gm, &scalars})
+                      &part_up, &dots, &gm, &scalars, &rein})
       b->release();
   }
   DevState* st() const { return state.as<DevState>(); }
@@ -563,10 +564,18 @@ void enqueue_iteration(lsopc_session* ss, int par, cudaStream_t s, cudaEvent_t* 
   launch_ls_velocity(g.H, g.W, ss->phi.as<double>(), v, dprev, ss->have_mod ? ss->mod.as<double>() : nullptr,
                      c.curvature_weight, c.use_curvature, st, d, ss->u.as<double>(),
                      c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), full_tile(g.W), s,
-                     &tail);
+                     &tail, c.grad_scheme == 1);
   launch_ls_update(g.H, g.W, ss->phi.as<double>(), ss->u.as<double>(), c.update_form ? ss->gm.as<double>() : nullptr,
                    c.d_lower, c.d_upper, st, ss->mask.as<uint8_t>(),
                    ss->part_up.as<double>(), full_tile(g.W), s, &tail);
+  if (c.reinit_every > 0) {  // opt-in: phi <- TSDF(mask) after every reinit_every-th iteration
+    double* rp = ss->rein.as<double>();
+    int* skip = reinterpret_cast<int*>(rp + ls_blocks() + 1);
+    launch_reduce(RD_COUNTNEQ8, n, nullptr, nullptr, ss->mask.as<uint8_t>(), nullptr, rp, rp + ls_blocks(), s);
+    launch_reinit_gate(st, rp + ls_blocks(), (double)n, c.reinit_every, skip, s);
+    launch_tsdf(g.H, g.W, ss->mask.as<uint8_t>(), c.d_upper, c.d_lower, ss->phi.as<double>(), p->tsdf_i.as<int>(),
+                p->tsdf_f.as<double>(), s, skip);
+  }
   mark(8);
   ck_launch("dso iteration");
 }
@@ -613,7 +622,8 @@ void enqueue_phase(lsopc_session* ss, int phase, cudaStream_t s) {
       launch_after_grad(sc + 2, 1, c.cg_restart_every, st, s);
       launch_ls_velocity(g.H, g.W, ss->phi.as<double>(), v, dprev, ss->have_mod ? ss->mod.as<double>() : nullptr,
                          c.curvature_weight, c.use_curvature, st, d, ss->u.as<double>(),
-                         c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), t, s);
+                         c.update_form ? ss->gm.as<double>() : nullptr, ss->part_ls.as<double>(), t, s, nullptr,
+                         c.grad_scheme == 1);
       launch_reduce_partials(ss->part_ls.as<double>(), ls_blocks(), 2, 1, sc + 4, s);
     } break;
     case 3: {  // CFL step on the global max; interior update -> max step
@@ -670,6 +680,8 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
     if (!cfg || !out) throw Error(LSOPC_EINVAL, "null argument");
     if (cfg->max_iters < 0) throw Error(LSOPC_EINVAL, "max_iters must be >= 0");
     if (cfg->cg_restart_every < 1) throw Error(LSOPC_EINVAL, "cg_restart_every must be >= 1");
+    if (cfg->grad_scheme != 0 && cfg->grad_scheme != 1) throw Error(LSOPC_EINVAL, "grad_scheme must be 0 or 1");
+    if (cfg->reinit_every < 0) throw Error(LSOPC_EINVAL, "reinit_every must be >= 0");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Grid& g = plan->g;
     const size_t n = g.n();
@@ -704,6 +716,11 @@ int lsopc_session_create(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_
         ss->part_up.ensure((size_t)ls_blocks() * sizeof(double));
         ss->dots.ensure((size_t)(finish_max_blocks() + 1) * 2 * sizeof(double));
         if (mod_dev) ss->mod.ensure(n * 8);
+        if (cfg->reinit_every > 0) ss->rein.ensure(((size_t)ls_blocks() + 2) * sizeof(double));
+      }
+      if (cfg->reinit_every > 0) {
+        plan->tsdf_i.ensure(tsdf_scratch_i32(g.H, g.W) * sizeof(int));
+        plan->tsdf_f.ensure(tsdf_scratch_f64(g.H, g.W) * sizeof(double));
       }
       ck(cudaMemcpyAsync(ss->target.p, target_dev, n, cudaMemcpyDeviceToDevice, s), "memcpy");
       launch_binarize_u8(n, ss->target.as<uint8_t>(), s);  // any non-zero byte is lit (optimizer.py:197)
@@ -880,6 +897,7 @@ int lsopc_session_set_tile(lsopc_session* ss, int ix0, int ix1, int xlo, int xhi
     if (!(0 <= ix0 && ix0 < ix1 && ix1 <= W && 0 <= xlo && xlo <= ix0 && ix1 <= xhi && xhi <= W))
       throw Error(LSOPC_EINVAL, "bad strip geometry");
     if (ss->it) throw Error(LSOPC_EINVAL, "set the strip before the first iteration");
+    if (ss->cfg.reinit_every > 0) throw Error(LSOPC_EINVAL, "reinitialisation needs the whole grid (not a strip)");
     ss->tiled = true;
     ss->tile = Tile{ix0, ix1, xlo, xhi};
     ss->scalars.ensure(8 * sizeof(double));
@@ -926,8 +944,9 @@ int lsopc_session_time_passes(lsopc_session* ss, int reps, double* ms_out) {
 int lsopc_session_launches_per_iter(const lsopc_session* ss) {
   if (!ss) return 0;
   // mask rows+cols 2, F1 1, F2 1, resist (+ loss control) 1, copy_best 1, A1 1, A2 1,
-  // A3 (+ CG control) 1, velocity (+ CFL control) 1, update (+ record) 1
-  return 2 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1;
+  // A3 (+ CG control) 1, velocity (+ CFL control) 1, update (+ record) 1;
+  // opt-in reinitialisation: lit count 2, gate 1, TSDF 3
+  return 2 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + (ss->cfg.reinit_every > 0 ? 6 : 0);
 }
 
 int lsopc_optimize(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_kset* defocus, const uint8_t* target_dev,

@@ -54,7 +54,8 @@ __device__ __forceinline__ double tsdf_value(D best, D clip, bool lit, double d_
 // g layout: g[f][y][x], f = 0: distance to the nearest lit pixel (mask != 0),
 // f = 1: distance to the nearest dark pixel.  seg[f][s][x] = {first, last}
 // feature row inside segment s (or -1).
-__global__ void k_edt_cols_local(int H, int W, const uint8_t* __restrict__ mask, int* g, int2* seg) {
+__global__ void k_edt_cols_local(int H, int W, const uint8_t* __restrict__ mask, int* g, int2* seg, const int* skip) {
+  if (skip && *skip) return;  // reinitialisation gate (lsopc loop)
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = blockIdx.y;
   if (x >= W) return;
@@ -84,7 +85,8 @@ __global__ void k_edt_cols_local(int H, int W, const uint8_t* __restrict__ mask,
 }
 
 // fold in the nearest feature rows of the other segments of the column
-__global__ void k_edt_cols_fix(int H, int W, const int2* __restrict__ seg, int* g) {
+__global__ void k_edt_cols_fix(int H, int W, const int2* __restrict__ seg, int* g, const int* skip) {
+  if (skip && *skip) return;  // reinitialisation gate (lsopc loop)
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = blockIdx.y;
   if (x >= W) return;
@@ -108,7 +110,8 @@ __global__ void k_edt_cols_fix(int H, int W, const int2* __restrict__ seg, int* 
 // nearest feature rows outside each segment, nb[f][s][x] = {last feature row
 // above the segment, first below it} (-1: none); the staged row pass folds
 // them into g as it loads a row, in place of k_edt_cols_fix
-__global__ void k_edt_cols_near(int W, const int2* __restrict__ seg, int2* nb) {
+__global__ void k_edt_cols_near(int W, const int2* __restrict__ seg, int2* nb, const int* skip) {
+  if (skip && *skip) return;  // reinitialisation gate (lsopc loop)
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = blockIdx.y, f = blockIdx.z;
   if (x >= W) return;
@@ -131,7 +134,8 @@ __global__ void k_edt_cols_near(int W, const int2* __restrict__ seg, int2* nb) {
 template <typename D>  // D: unsigned when every squared distance fits (sides <= 32768), else long long
 __global__ void __launch_bounds__(256) k_edt_rows_scan(int H, int W, const uint8_t* __restrict__ mask,
                                                       const int* __restrict__ g, D clip_dark, D clip_lit,
-                                                      double d_upper, double d_lower, double* phi) {
+                                                      double d_upper, double d_lower, double* phi, const int* skip) {
+  if (skip && *skip) return;  // reinitialisation gate (lsopc loop)
   const int y = blockIdx.x;
   const int* g1 = g + (size_t)y * W;                   // f = 0: distance to the nearest lit pixel
   const int* g0 = g + (size_t)H * W + (size_t)y * W;   // f = 1: distance to the nearest dark pixel
@@ -174,7 +178,8 @@ __global__ void __launch_bounds__(LSB_TSDF_THREADS) k_edt_rows_pruned(int H, int
                                                                       const int* __restrict__ g,
                                                                       const int2* __restrict__ nb, D clip_dark,
                                                                       D clip_lit, double d_upper, double d_lower,
-                                                                      double* phi) {
+                                                                      double* phi, const int* skip) {
+  if (skip && *skip) return;  // reinitialisation gate (lsopc loop)
   constexpr int kChunk = LSB_TSDF_CHUNK, kNear = LSB_TSDF_NEAR;  // kChunk divides 32
   constexpr int kSuper = LSB_TSDF_SUPER, kPer = kSuper / kChunk;  // super-chunk = kPer chunks
   // no feature in the column; sums with any offset^2 stay below overflow
@@ -308,13 +313,13 @@ size_t tsdf_scratch_i32(int H, int W) {
 size_t tsdf_scratch_f64(int H, int W) { return 1; }
 
 void launch_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_lower, double* phi,
-                 int* si, double* sf, cudaStream_t s) {
+                 int* si, double* sf, cudaStream_t s, const int* skip) {
   (void)sf;
   int* g = si;
   int2* seg = reinterpret_cast<int2*>(si + (size_t)2 * H * W);
   int2* nb = seg + (size_t)2 * kSegs * W;
   const dim3 cg((W + 127) / 128, kSegs);
-  k_edt_cols_local<<<cg, 128, 0, s>>>(H, W, mask, g, seg);
+  k_edt_cols_local<<<cg, 128, 0, s>>>(H, W, mask, g, seg, skip);
   // dark pixels: value d - 0.5 reaches D_u; lit pixels: -(d - 0.5) reaches D_l
   const long long clip_dark = clip_d2(d_upper + 0.5), clip_lit = clip_d2(0.5 - d_lower);
   const bool narrow = H <= 32768 && W <= 32768;  // t^2 + g^2 < 2^31
@@ -324,13 +329,13 @@ void launch_tsdf(int H, int W, const uint8_t* mask, double d_upper, double d_low
     const D cd = (D)std::min<long long>(clip_dark, big), cl = (D)std::min<long long>(clip_lit, big);
     const size_t sm = tsdf_row_smem(W, sizeof(D));
     if (sm <= 200 * 1024) {
-      k_edt_cols_near<<<dim3((W + 127) / 128, kSegs, 2), 128, 0, s>>>(W, seg, nb);
+      k_edt_cols_near<<<dim3((W + 127) / 128, kSegs, 2), 128, 0, s>>>(W, seg, nb, skip);
       auto k = k_edt_rows_pruned<D>;
       if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k<<<H, LSB_TSDF_THREADS, sm, s>>>(H, W, mask, g, nb, cd, cl, d_upper, d_lower, phi);
+      k<<<H, LSB_TSDF_THREADS, sm, s>>>(H, W, mask, g, nb, cd, cl, d_upper, d_lower, phi, skip);
     } else {  // rows too wide to stage: fix g in place, scan it in global memory
-      k_edt_cols_fix<<<cg, 128, 0, s>>>(H, W, seg, g);
-      k_edt_rows_scan<D><<<H, 256, 0, s>>>(H, W, mask, g, cd, cl, d_upper, d_lower, phi);
+      k_edt_cols_fix<<<cg, 128, 0, s>>>(H, W, seg, g, skip);
+      k_edt_rows_scan<D><<<H, 256, 0, s>>>(H, W, mask, g, cd, cl, d_upper, d_lower, phi, skip);
     }
   };
   if (narrow) run(0u);

@@ -14,7 +14,7 @@ import numpy as np
 
 from . import _native as nv
 
-__all__ = ["MetricsReport", "l2_error", "pvband", "fracture", "shot_count"]
+__all__ = ["MetricsReport", "l2_error", "pvband", "fracture", "shot_count", "EPEReport", "epe"]
 
 
 @dataclass
@@ -130,3 +130,54 @@ def shot_count(mask):
     nv.check(nv.lib().lsopc_fracture(m.shape[0], m.shape[1], m.ctypes.data_as(ctypes.c_void_p),
                                      None, 0, ctypes.byref(count)))
     return int(count.value)
+
+
+# ---------------------------------------------------------------------------
+# EXTENSION: edge placement error (the reference has none; parity
+# is UNPINNED -- checked against oracle/lsopc_oracle.py `epe` only)
+
+
+@dataclass
+class EPEReport:
+    """EPE on the target's edges (ICCAD-2013 style): `samples` measured,
+    `violations` with |EPE| > threshold, mean and max |EPE| (pixels; |EPE|
+    saturates at threshold + 1)."""
+    samples: int
+    violations: int
+    mean_abs: float
+    max_abs: int
+    spacing: int = 40
+    threshold: int = 15
+
+    def as_dict(self):
+        return {"samples": self.samples, "violations": self.violations, "mean_abs": self.mean_abs,
+                "max_abs": self.max_abs, "spacing": self.spacing, "threshold": self.threshold,
+                "parity": "unpinned (no reference EPE)"}
+
+
+def epe(printed, target, spacing=40, threshold=15, offset=None):
+    """Edge placement error of a hard print against the target layout
+    (lsopc_epe; see include/lsopc_b200.h for the definition): samples every
+    `spacing` pixels on a lattice along the target's edges, the printed
+    edge's signed displacement along the outward normal, violations where
+    |EPE| > `threshold` (defaults: 40 / 15 px, the ICCAD-2013 nm figures at
+    1 nm pitch).  Host or device uint8 / bool grids."""
+    t = nv.torch()
+    if offset is None:
+        offset = spacing // 2
+
+    def dev(a):
+        if _is_device(a):
+            return _device_u8(a)
+        return nv.to_dev(np.not_equal(np.asarray(a), 0).view(np.uint8), np.uint8)
+
+    p, g = dev(printed), dev(target)
+    if tuple(p.shape) != tuple(g.shape) or p.dim() != 2:
+        raise ValueError(f"dimension mismatch: {tuple(p.shape)} vs {tuple(g.shape)}")
+    out = (ctypes.c_double * 4)()
+    nv.check(nv.lib().lsopc_epe(p.shape[0], p.shape[1], nv.ptr(p), nv.ptr(g), int(spacing), int(offset),
+                                int(threshold), int(threshold) + 1, out, nv.stream()))
+    del t
+    n = int(out[0])
+    return EPEReport(samples=n, violations=int(out[1]), mean_abs=(out[2] / n if n else 0.0), max_abs=int(out[3]),
+                     spacing=int(spacing), threshold=int(threshold))

@@ -56,6 +56,12 @@ class OptConfig:
     grid_side: int = 0
     cg_restart_every: int = 50
     precision: str = None
+    # opt-in extensions, off by default (the reference has neither): the
+    # Godunov upwind |grad phi| in the update term ("upwind") instead of the
+    # central one (levelset.py:60-62), and phi <- tsdf(mask_from_phi(phi))
+    # after every `reinit_every`-th completed iteration
+    grad_scheme: str = "central"
+    reinit_every: int = 0
 
     def __post_init__(self):
         if self.alpha < 0 or self.beta < 0 or (self.alpha == 0 and self.beta == 0):
@@ -68,6 +74,10 @@ class OptConfig:
             raise ValueError("max_iters must be >= 0")
         if self.precision is not None and str(self.precision).lower() not in ("fp32", "fp64"):
             raise ValueError("precision must be fp32, fp64 or None")
+        if self.grad_scheme not in ("central", "upwind"):
+            raise ValueError("grad_scheme must be central or upwind")
+        if self.reinit_every < 0:
+            raise ValueError("reinit_every must be >= 0")
 
 
 @dataclass
@@ -237,6 +247,8 @@ def _native_cfg(cfg, max_iters=None, stop_patience=None, use_curvature=None, upd
     c.use_curvature = int(bool(cfg.use_curvature if use_curvature is None else use_curvature))
     c.cg_restart_every = int(cfg.cg_restart_every)
     c.update_form = int(update_form)
+    c.grad_scheme = 1 if getattr(cfg, "grad_scheme", "central") == "upwind" else 0
+    c.reinit_every = int(getattr(cfg, "reinit_every", 0))
     return c
 
 
