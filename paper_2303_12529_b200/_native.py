@@ -303,7 +303,10 @@ def plan_for(shape, prec):
 
 
 class DeviceKernelSet:
-    """Device spectra of one KernelSet on one plan (litho.py:71-82 cache)."""
+    """Device spectra of one KernelSet on one plan (litho.py:71-82 cache).
+    `builds` counts spectra builds (K0) in this process."""
+
+    builds = 0
 
     def __init__(self, plan, coeffs, weights):
         self.plan = plan
@@ -315,6 +318,7 @@ class DeviceKernelSet:
                                       stream(), ctypes.byref(h)))
         self.handle = h
         self.nk = c.shape[0]
+        DeviceKernelSet.builds += 1
 
     def __del__(self):
         try:

@@ -2,8 +2,7 @@
 # Dev validation (not part of the driver's tests): run the reference package's
 # own pytest suite against the B200 drop-in through an `lsopc` shim.
 #   prep  (build container, where /root/reference exists): copies the reference
-#         tests and its host-only cli.py / fileio.py into the git-ignored
-#         baseline/_ref/ (never committed)
+#         tests into the git-ignored baseline/_ref/ (never committed)
 #   run   (GPU box): pytest with the shim first on PYTHONPATH
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
@@ -13,16 +12,14 @@ case "$1" in
     rm -rf "$REF/tests" "$REF/shim"
     mkdir -p "$REF/shim/lsopc"
     cp -r /root/reference/pkg/tests "$REF/tests"
-    cp /root/reference/pkg/src/lsopc/cli.py /root/reference/pkg/src/lsopc/fileio.py "$REF/shim/lsopc/"
     cat > "$REF/shim/lsopc/__init__.py" <<'PY'
-# shim: `import lsopc` -> the B200 drop-in; cli/fileio stay the reference's host code
+# shim: `import lsopc` -> the B200 drop-in, every module including cli / fileio
 import sys
 import paper_2303_12529_b200 as _b2
 from paper_2303_12529_b200 import *  # noqa
-from paper_2303_12529_b200 import errors, fields, levelset, litho, metrics, optimizer  # noqa
-for _m in ("errors", "fields", "levelset", "litho", "metrics", "optimizer"):
+from paper_2303_12529_b200 import cli, errors, fields, fileio, levelset, litho, metrics, optimizer  # noqa
+for _m in ("cli", "errors", "fields", "fileio", "levelset", "litho", "metrics", "optimizer"):
     sys.modules["lsopc." + _m] = getattr(_b2, _m)
-from . import fileio, cli  # noqa: E402  (reference host code on top of the drop-in)
 PY
     echo "prepared $REF" ;;
   run)
