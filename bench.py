@@ -468,12 +468,12 @@ def b200_arm(args, world, rank, local):
                                                                   precision=args.precision))  # warm-up
         rt = tiled.optimize_tiled(mosaic, focus, defocus, cfg_t)
         loop = parallel.max_over_ranks(rt.loop_time, device="cuda")
-        st = tiled.strip_geometry(T, T, world, rank, K_SIDE)
-        tile = {"side": T, "ranks": world, "window": [T, st.ww], "iters": rt.iters_run,
+        st = tiled.strip_geometry(T, T, world, rank, K_SIDE, axis=0)
+        tile = {"side": T, "ranks": world, "window": list(st.window_shape), "iters": rt.iters_run,
                 "loop_s": round(loop, 4), "iters_per_s": round(rt.iters_run / loop, 3),
                 "ms_per_iter": round(1e3 * loop / rt.iters_run, 2),
-                "note": f"{T}^2 mosaic of iccad_like_clips, full-height strips over {world} rank(s), "
-                        "34-column phi halo exchange + 4 scalar all-reduces per iteration (configs[4])"}
+                "note": f"{T}^2 mosaic of iccad_like_clips, full-width row strips over {world} rank(s), "
+                        "34-row phi halo exchange + 4 scalar all-reduces per iteration (configs[4])"}
 
     # ---- the reference's own precision (fp64 tier: complex128 transforms) -----
     tiers = {}

@@ -209,6 +209,12 @@ int lsopc_dsn_init(size_t n, const float* phi_raw_dev, const float* m_raw_dev, d
  * refreshes the halo columns of lsopc_session_phi_ptr().  Forward phases
  * threshold phi directly, so only phi needs exchanging. */
 int lsopc_session_set_tile(lsopc_session* s, int ix0, int ix1, int xlo, int xhi);
+/* The general strip window: interior [iy0, iy1) x [ix0, ix1), stencil
+ * neighbours bounded by [ylo, yhi) x [xlo, xhi).  Full-width strips (rows
+ * of the tile, iy-ranges) keep the long 8192-point axis on the rows, whose
+ * transforms stream by TMA; set_tile is the full-height special case. */
+int lsopc_session_set_window(lsopc_session* s, int ix0, int ix1, int xlo, int xhi, int iy0, int iy1, int ylo,
+                             int yhi);
 int lsopc_session_phase(lsopc_session* s, int phase);
 double* lsopc_session_scalars(lsopc_session* s);
 double* lsopc_session_phi_ptr(lsopc_session* s);

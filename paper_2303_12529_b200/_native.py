@@ -83,6 +83,7 @@ _SIGS = {
     "lsopc_epe": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, ctypes.POINTER(_D), _P]),
     "lsopc_session_time_passes": (_I, [_P, _I, ctypes.POINTER(_D)]),
     "lsopc_session_set_tile": (_I, [_P, _I, _I, _I, _I]),
+    "lsopc_session_set_window": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I]),
     "lsopc_dsn_init": (_I, [_Z, _P, _P, _D, _D, _D, _P, _P, _P]),
     "lsopc_session_phase": (_I, [_P, _I]),
     "lsopc_session_scalars": (_P, [_P]),

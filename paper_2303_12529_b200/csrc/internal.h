@@ -78,7 +78,7 @@ struct LoopTail;  // internal_ls.h
 int launch_adjoint_finish(const Grid& g, const void* V0, const void* V1, double scale, double* out,
                           const double* v_prev, double* dots, StopFlag stop, cudaStream_t s, int ix0 = 0,
                           int ix1 = 0,  // dots over columns [ix0, ix1) (0, 0: all)
-                          const LoopTail* tail = nullptr);
+                          const LoopTail* tail = nullptr, int iy0 = 0, int iy1 = 1 << 30);  // ... rows [iy0, iy1)
 int finish_max_blocks();
 
 // ---- elementwise / reductions ---------------------------------------------------
@@ -95,7 +95,8 @@ void launch_resist(const Grid& g, const void* If, const void* Id, const uint8_t*
                    double* z_nom, double* z_in, double* z_out, uint8_t* h_nom,
                    uint8_t* h_in, uint8_t* h_out, double* partials, StopFlag stop,
                    cudaStream_t s, int ix0 = 0, int ix1 = 0,  // losses over columns [ix0, ix1) (0, 0: all)
-                   const LoopTail* tail = nullptr);  // after_forward fused into the DSO loop form
+                   const LoopTail* tail = nullptr,   // after_forward fused into the DSO loop form
+                   int iy0 = 0, int iy1 = 1 << 30);   // ... and rows [iy0, iy1)
 // single-corner intensity output: out = max(dose * I, 0) (f64)
 void launch_scale_intensity(const Grid& g, const void* I, double dose, double* out, cudaStream_t s);
 // gate for a user-supplied print: w = scale * (z - zt) z (1 - z)   (element R)

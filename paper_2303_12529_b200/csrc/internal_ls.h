@@ -23,13 +23,16 @@ struct DevState {
   unsigned ticket[4];  // last-block tickets of the fused control tails (control.cuh), zero between launches
 };
 
-// Column ranges (window coordinates) of a strip of an oversized tile run on
-// one rank: [ix0, ix1) is the interior this rank owns (losses, dots, maxima,
-// updates), [xlo, xhi) bounds the x-neighbours of the phi stencil (replicate
-// padding at the global tile edge, halo data elsewhere).  The default covers
-// the whole grid.
+// Window of a strip of an oversized tile run on one rank (window
+// coordinates): [iy0, iy1) x [ix0, ix1) is the interior this rank owns
+// (losses, dots, maxima, updates), [ylo, yhi) x [xlo, xhi) bounds the
+// neighbours of the phi stencil (replicate padding at the global tile edge,
+// halo data elsewhere).  Strips are full-width (rows) or full-height
+// (columns); the row fields default to the whole grid (kAll is clamped to H).
+constexpr int kAll = 1 << 30;
 struct Tile {
   int ix0, ix1, xlo, xhi;
+  int iy0 = 0, iy1 = kAll, ylo = 0, yhi = kAll;
 };
 inline Tile full_tile(int W) { return Tile{0, W, 0, W}; }
 
@@ -77,9 +80,10 @@ void launch_after_velocity(const double* part, int nb, double eta, DevState* st,
 void launch_after_update(const double* part, int nb, DevState* st, double* hist, cudaStream_t s);
 void launch_elementwise(int op, size_t n, const double* a, const double* b, double p0, double p1, double p2,
                         double* out, uint8_t* out8, cudaStream_t s);
-// out: device scalar.  W > 0 restricts RD_COUNTNEQ8 to columns [ix0, ix1) of rows of width W.
+// out: device scalar.  W > 0 restricts RD_COUNTNEQ8 to columns [ix0, ix1) x rows [iy0, iy1) of rows of width W.
 void launch_reduce(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
-                   double* partials, double* out, cudaStream_t s, int W = 0, int ix0 = 0, int ix1 = 0);
+                   double* partials, double* out, cudaStream_t s, int W = 0, int ix0 = 0, int ix1 = 0,
+                   int iy0 = 0, int iy1 = kAll);
 
 // p[i] = p[i] != 0 (uint8, in place; 16-byte aligned p)
 void launch_binarize_u8(size_t n, uint8_t* p, cudaStream_t s);

@@ -70,10 +70,12 @@ struct Geom {
 
 // levelset.py:112-118, replicate ("edge") padding; x-neighbours clamped to
 // [xlo, xhi) (the whole row unless the grid is a strip of a larger tile)
-LS_D Geom geometry_at(const double* __restrict__ phi, int H, int W, int y, int x, int xlo = 0, int xhi = -1) {
+LS_D Geom geometry_at(const double* __restrict__ phi, int H, int W, int y, int x, int xlo = 0, int xhi = -1,
+                      int ylo = 0, int yhi = -1) {
   if (xhi < 0) xhi = W;
+  if (yhi < 0 || yhi > H) yhi = H;
   const int xe = x + 1 < xhi ? x + 1 : xhi - 1, xw = x > xlo ? x - 1 : xlo;
-  const int ys = y + 1 < H ? y + 1 : H - 1, yn = y > 0 ? y - 1 : 0;
+  const int ys = y + 1 < yhi ? y + 1 : yhi - 1, yn = y > ylo ? y - 1 : ylo;
   const double* r = phi + (size_t)y * W;
   const double* rs = phi + (size_t)ys * W;
   const double* rn = phi + (size_t)yn * W;
@@ -149,9 +151,10 @@ LS_D double upwind_mag(const VelIn& a, double F) {
 }
 
 // one-sided differences at (y, x) with the stencil's clamps (slow path)
-LS_D void one_sided_at(const double* __restrict__ phi, int H, int W, int y, int x, int xlo, int xhi, VelIn& a) {
+LS_D void one_sided_at(const double* __restrict__ phi, int H, int W, int y, int x, int xlo, int xhi, int ylo,
+                       int yhi, VelIn& a) {
   const int xe = x + 1 < xhi ? x + 1 : xhi - 1, xw = x > xlo ? x - 1 : xlo;
-  const int ys = y + 1 < H ? y + 1 : H - 1, yn = y > 0 ? y - 1 : 0;
+  const int ys = y + 1 < yhi ? y + 1 : yhi - 1, yn = y > ylo ? y - 1 : ylo;
   const double c = phi[(size_t)y * W + x];
   a.dmx = sub(c, phi[(size_t)y * W + xw]);
   a.dpx = sub(phi[(size_t)y * W + xe], c);
@@ -197,12 +200,14 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
   const size_t n2 = (size_t)H * W / 2;
   double mx[2] = {0.0, 0.0};  // max |v_total|, max |grad phi|
   const RowSplit rs = row_split(W);
+  const int yhi = tl.yhi < H ? tl.yhi : H, ylo = tl.ylo;
+  const int iy1 = tl.iy1 < H ? tl.iy1 : H;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n2; q += (size_t)gridDim.x * blockDim.x) {
     const size_t i = 2 * q;
     const int y = (int)row_of(rs, i), x = (int)col_of(rs, i);
     VelIn a[2];
     if (x - 1 >= tl.xlo && x + 2 < tl.xhi) {
-      const int ys = y + 1 < H ? y + 1 : H - 1, yn = y > 0 ? y - 1 : 0;
+      const int ys = y + 1 < yhi ? y + 1 : yhi - 1, yn = y > ylo ? y - 1 : ylo;
       const double* r = phi + (size_t)y * W + x;
       const double* rS = phi + (size_t)ys * W + x;
       const double* rN = phi + (size_t)yn * W + x;
@@ -228,11 +233,11 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
         }
       }
     } else {
-      a[0].g = geometry_at(phi, H, W, y, x, tl.xlo, tl.xhi);
-      a[1].g = geometry_at(phi, H, W, y, x + 1, tl.xlo, tl.xhi);
+      a[0].g = geometry_at(phi, H, W, y, x, tl.xlo, tl.xhi, ylo, yhi);
+      a[1].g = geometry_at(phi, H, W, y, x + 1, tl.xlo, tl.xhi, ylo, yhi);
       if (upwind) {
-        one_sided_at(phi, H, W, y, x, tl.xlo, tl.xhi, a[0]);
-        one_sided_at(phi, H, W, y, x + 1, tl.xlo, tl.xhi, a[1]);
+        one_sided_at(phi, H, W, y, x, tl.xlo, tl.xhi, ylo, yhi, a[0]);
+        one_sided_at(phi, H, W, y, x + 1, tl.xlo, tl.xhi, ylo, yhi, a[1]);
       }
     }
     const double2 vv = *reinterpret_cast<const double2*>(v + i);
@@ -265,7 +270,7 @@ k_ls_velocity(int H, int W, const double* __restrict__ phi, const double* __rest
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      if (x + e >= tl.ix0 && x + e < tl.ix1) {
+      if (x + e >= tl.ix0 && x + e < tl.ix1 && y >= tl.iy0 && y < iy1) {
         mx[0] = nmax(mx[0], fabs(vt[e]));
         mx[1] = nmax(mx[1], gm[e]);
       }
@@ -294,7 +299,8 @@ k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const doubl
   const size_t n4 = (size_t)H * W / 4;
   double mx[1] = {0.0};
   const RowSplit rs = row_split(W);
-  const bool whole = tl.ix0 <= 0 && tl.ix1 >= W;
+  const bool all_rows = tl.iy0 <= 0 && tl.iy1 >= H;
+  const bool whole = tl.ix0 <= 0 && tl.ix1 >= W && all_rows;
   auto one = [&](double ph, double uu, double gg, double& step) {
     if (gm) {  // optimizer.py:329: phi - dt * v_total * grad_mag
       step = mul(mul(dt, uu), gg);
@@ -306,7 +312,8 @@ k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const doubl
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n4; q += (size_t)gridDim.x * blockDim.x) {
     const size_t i = 4 * q;
     const int x = whole ? 0 : (int)col_of(rs, i);
-    if (whole || (x >= tl.ix0 && x + 4 <= tl.ix1)) {
+    const bool row_in = all_rows || ((int)row_of(rs, i) >= tl.iy0 && (int)row_of(rs, i) < tl.iy1);
+    if (whole || (row_in && x >= tl.ix0 && x + 4 <= tl.ix1)) {
       const double2 p0 = *reinterpret_cast<const double2*>(phi + i), p1 = *reinterpret_cast<const double2*>(phi + i + 2);
       const double2 u0 = *reinterpret_cast<const double2*>(u + i), u1 = *reinterpret_cast<const double2*>(u + i + 2);
       double2 g0 = make_double2(0.0, 0.0), g1 = g0;
@@ -323,7 +330,7 @@ k_ls_update(int H, int W, double* phi, const double* __restrict__ u, const doubl
       mx[0] = nmax(nmax(nmax(mx[0], fabs(s0)), nmax(fabs(s1), fabs(s2))), fabs(s3));
     } else {
       for (int e = 0; e < 4; ++e) {
-        if (x + e < tl.ix0 || x + e >= tl.ix1) continue;  // strip halo: owned by a neighbour rank
+        if (!row_in || x + e < tl.ix0 || x + e >= tl.ix1) continue;  // strip halo: owned by a neighbour rank
         double step;
         const double p = one(phi[i + e], u[i + e], gm ? gm[i + e] : 0.0, step);
         phi[i + e] = p;
@@ -432,7 +439,8 @@ __global__ void k_dsn_init(size_t n, const float* __restrict__ phi_raw, const fl
 
 __global__ void __launch_bounds__(kThreads)
 k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restrict__ b,
-         const uint8_t* __restrict__ a8, const uint8_t* __restrict__ b8, double* partials, int W, int ix0, int ix1) {
+         const uint8_t* __restrict__ a8, const uint8_t* __restrict__ b8, double* partials, int W, int ix0, int ix1,
+         int iy0, int iy1) {
   __shared__ double red[32];
   double acc[1] = {0.0};
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -441,10 +449,10 @@ k_reduce(int op, size_t n, const double* __restrict__ a, const double* __restric
       case RD_DOT: acc[0] += a[i] * b[i]; break;
       case RD_DOTDIFF: acc[0] += a[i] * (a[i] - b[i]); break;
       case RD_MAXABS: acc[0] = nmax(acc[0], fabs(a[i])); break;
-      case RD_COUNTNEQ8:  // b8 null: vs 0; W > 0: columns [ix0, ix1) only
+      case RD_COUNTNEQ8:  // b8 null: vs 0; W > 0: columns [ix0, ix1) x rows [iy0, iy1) only
         if (W > 0) {
-          const int x = (int)col_of(row_split(W), i);
-          if (x < ix0 || x >= ix1) break;
+          const int x = (int)col_of(row_split(W), i), y = (int)row_of(row_split(W), i);
+          if (x < ix0 || x >= ix1 || y < iy0 || y >= iy1) break;
         }
         acc[0] += (a8[i] != (b8 ? b8[i] : 0)) ? 1.0 : 0.0;
         break;
@@ -545,8 +553,8 @@ void launch_binarize_u8(size_t n, uint8_t* p, cudaStream_t s) {
   k_binarize_u8<<<kBlocks, kThreads, 0, s>>>(n, p);
 }
 void launch_reduce(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
-                   double* partials, double* out, cudaStream_t s, int W, int ix0, int ix1) {
-  k_reduce<<<kBlocks, kThreads, 0, s>>>(op, n, a, b, a8, b8, partials, W, ix0, ix1);
+                   double* partials, double* out, cudaStream_t s, int W, int ix0, int ix1, int iy0, int iy1) {
+  k_reduce<<<kBlocks, kThreads, 0, s>>>(op, n, a, b, a8, b8, partials, W, ix0, ix1, iy0, iy1);
   k_reduce_final<<<1, 256, 0, s>>>(op, partials, kBlocks, out);
 }
 

@@ -119,7 +119,7 @@ void check_kset(const lsopc_plan* p, const lsopc_kset* k) {
 }
 
 double reduce_to_host(int op, size_t n, const double* a, const double* b, const uint8_t* a8, const uint8_t* b8,
-                      lsopc_plan* plan, cudaStream_t s, int W = 0, int ix0 = 0, int ix1 = 0) {
+                      lsopc_plan* plan, cudaStream_t s, int W = 0, Tile t = Tile{0, 0, 0, 0}) {
   thread_local DevBuf tmp;  // plan-less calls: per-thread partials, kept across calls
   double* part;
   double* out;
@@ -131,7 +131,7 @@ double reduce_to_host(int op, size_t n, const double* a, const double* b, const 
     part = tmp.as<double>();
     out = part + ls_blocks();
   }
-  launch_reduce(op, n, a, b, a8, b8, part, out, s, W, ix0, ix1);
+  launch_reduce(op, n, a, b, a8, b8, part, out, s, W, t.ix0, t.ix1, t.iy0, t.iy1);
   ck_launch("reduce");
   double h = 0.0;
   ck(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, s), "memcpy");
@@ -605,7 +605,8 @@ void enqueue_phase(lsopc_session* ss, int phase, cudaStream_t s) {
       launch_f2(g, sets, 2, nullptr, stop, s);
       ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
       launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr,
-                    nullptr, nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s, t.ix0, t.ix1);
+                    nullptr, nullptr, nullptr, nullptr, nullptr, p->partials.as<double>(), stop, s, t.ix0, t.ix1,
+                    nullptr, t.iy0, t.iy1);
       launch_reduce_partials(p->partials.as<double>(), reduce_blocks(), 4, 0, sc, s);
     } break;
     case 1: {  // stop rule on the global losses; adjoint -> sum PR dots
@@ -615,7 +616,7 @@ void enqueue_phase(lsopc_session* ss, int phase, cudaStream_t s) {
       launch_a1(g, sets, 2, stop, s);
       launch_a2(g, sets, 2, stop, s);
       const int nd = launch_adjoint_finish(g, p->V0.p, p->V1.p, 4.0 * c.sigma_z / (double)n, v, vprev,
-                                           ss->dots.as<double>(), stop, s, t.ix0, t.ix1);
+                                           ss->dots.as<double>(), stop, s, t.ix0, t.ix1, nullptr, t.iy0, t.iy1);
       launch_reduce_partials(ss->dots.as<double>(), nd, 2, 0, sc + 2, s);
     } break;
     case 2: {  // CG on the global dots; level-set velocity -> max |v_total|, max |grad phi|
@@ -820,10 +821,8 @@ int lsopc_session_finish(lsopc_session* ss, double* best_phi_dev, uint8_t* final
                     hn + n, hn + 2 * n, nullptr, nullptr, s);
       ck_launch("final prints");
       const int cw = ss->tiled ? g.W : 0;  // strip: count the interior columns only
-      l2 = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn, ss->target.as<uint8_t>(), p, s, cw, ss->tile.ix0,
-                          ss->tile.ix1);
-      pvb = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn + n, hn + 2 * n, p, s, cw, ss->tile.ix0,
-                           ss->tile.ix1);
+      l2 = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn, ss->target.as<uint8_t>(), p, s, cw, ss->tile);
+      pvb = reduce_to_host(RD_COUNTNEQ8, n, nullptr, nullptr, hn + n, hn + 2 * n, p, s, cw, ss->tile);
     }
     if (best_phi_dev) ck(cudaMemcpyAsync(best_phi_dev, ss->best.p, n * 8, cudaMemcpyDeviceToDevice, s), "memcpy");
     ck(cudaStreamSynchronize(s), "sync");
@@ -890,16 +889,19 @@ int lsopc_dsn_init(size_t n, const float* phi_raw_dev, const float* m_raw_dev, d
   });
 }
 
-int lsopc_session_set_tile(lsopc_session* ss, int ix0, int ix1, int xlo, int xhi) {
+int lsopc_session_set_window(lsopc_session* ss, int ix0, int ix1, int xlo, int xhi, int iy0, int iy1, int ylo,
+                             int yhi) {
   return guarded([&] {
     if (!ss) throw Error(LSOPC_EINVAL, "null session");
-    const int W = ss->plan->g.W;
+    const int W = ss->plan->g.W, H = ss->plan->g.H;
     if (!(0 <= ix0 && ix0 < ix1 && ix1 <= W && 0 <= xlo && xlo <= ix0 && ix1 <= xhi && xhi <= W))
-      throw Error(LSOPC_EINVAL, "bad strip geometry");
+      throw Error(LSOPC_EINVAL, "bad strip geometry (columns)");
+    if (!(0 <= iy0 && iy0 < iy1 && iy1 <= H && 0 <= ylo && ylo <= iy0 && iy1 <= yhi && yhi <= H))
+      throw Error(LSOPC_EINVAL, "bad strip geometry (rows)");
     if (ss->it) throw Error(LSOPC_EINVAL, "set the strip before the first iteration");
     if (ss->cfg.reinit_every > 0) throw Error(LSOPC_EINVAL, "reinitialisation needs the whole grid (not a strip)");
     ss->tiled = true;
-    ss->tile = Tile{ix0, ix1, xlo, xhi};
+    ss->tile = Tile{ix0, ix1, xlo, xhi, iy0, iy1, ylo, yhi};
     ss->scalars.ensure(8 * sizeof(double));
     ck(cudaMemsetAsync(ss->scalars.p, 0, 8 * sizeof(double), ss->s), "memset");
   });
@@ -913,6 +915,12 @@ int lsopc_session_phase(lsopc_session* ss, int phase) {
     enqueue_phase(ss, phase, ss->s);
     if (phase == 4) ++ss->it;
   });
+}
+
+int lsopc_session_set_tile(lsopc_session* ss, int ix0, int ix1, int xlo, int xhi) {
+  if (!ss) return lsopc_session_set_window(ss, ix0, ix1, xlo, xhi, 0, 1, 0, 1);
+  const int H = ss->plan->g.H;
+  return lsopc_session_set_window(ss, ix0, ix1, xlo, xhi, 0, H, 0, H);
 }
 
 double* lsopc_session_scalars(lsopc_session* ss) { return ss ? ss->scalars.as<double>() : nullptr; }

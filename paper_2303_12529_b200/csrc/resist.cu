@@ -28,13 +28,13 @@ __global__ void __launch_bounds__(kRedThreads)
 k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uint8_t* __restrict__ tu8,
          const double* __restrict__ tf, ResistParams p, R* wf, R* wd, double* z_nom, double* z_in,
          double* z_out, uint8_t* h_nom, uint8_t* h_in, uint8_t* h_out, double* partials,
-         StopFlag stop, int W, int ix0, int ix1) {
+         StopFlag stop, int W, int ix0, int ix1, int iy0, int iy1) {
   __shared__ double red[128];
   if (stop && *stop) return;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const bool have_t = tu8 || tf;
   const RowSplit rs = row_split(W);
-  const bool whole = ix0 <= 0 && ix1 >= W;
+  const bool whole = ix0 <= 0 && ix1 >= W && iy0 <= 0 && iy1 >= (int)(n / (size_t)W);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     // litho.py:125-126: I = max(dose * sum, 0); corners: litho.py:147-149
     double sf = (double)If[i];
@@ -58,8 +58,8 @@ k_resist(size_t n, const R* __restrict__ If, const R* __restrict__ Id, const uin
     if (have_t) {
       double zt = tu8 ? (double)tu8[i] : tf[i];
       double dn = zn - zt, di = zi - zt, dout = zo - zt;
-      const int x = whole ? ix0 : (int)col_of(rs, i);
-      if (x >= ix0 && x < ix1) {         // strip interior (the whole row by default)
+      const int x = whole ? ix0 : (int)col_of(rs, i), y = whole ? iy0 : (int)row_of(rs, i);
+      if (x >= ix0 && x < ix1 && y >= iy0 && y < iy1) {  // strip interior (the whole grid by default)
         acc[0] += dn * dn;               // optimizer.py:88-90
         acc[1] += di * di + dout * dout;  // optimizer.py:93-96
         // hard prints (litho.py:129-131): L2 vs the target, PVB inner vs outer (metrics.py:39-52)
@@ -107,12 +107,12 @@ template <typename R>
 __global__ void __launch_bounds__(kRedThreads)
 k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, const uint8_t* __restrict__ tu8,
               const double* __restrict__ tf, ResistParams p, R* wf, R* wd, double* partials, StopFlag stop, int W,
-              int ix0, int ix1, LoopTail tail) {
+              int ix0, int ix1, int iy0, int iy1, LoopTail tail) {
   __shared__ double red[128];
   if (stop && *stop) return;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const RowSplit rs = row_split(W);
-  const bool whole = ix0 <= 0 && ix1 >= W;
+  const bool whole = ix0 <= 0 && ix1 >= W && iy0 <= 0 && iy1 >= (int)(4 * n4 / (size_t)W);
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n4; g += (size_t)gridDim.x * blockDim.x) {
     const size_t i = 4 * g;
     R sf[4], sd[4] = {(R)0, (R)0, (R)0, (R)0};
@@ -128,6 +128,7 @@ k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, con
       ld4(tf, i, zt);
     }
     const int x0 = whole ? ix0 : (int)col_of(rs, i);
+    const bool row_in = whole || ((int)row_of(rs, i) >= iy0 && (int)row_of(rs, i) < iy1);
     R gf[4], gd[4];
     // float64 sigmoid and gates in both tiers: the loop's losses agree with the
     // API path (print_corners / ilt_loss) on the same intensities
@@ -139,7 +140,7 @@ k_resist_loop(size_t n4, const R* __restrict__ If, const R* __restrict__ Id, con
       const double zn = sigmoid(i_nom, p.i_th, p.sigma_z), zo = sigmoid(i_out, p.i_th, p.sigma_z),
                    zi = sigmoid(i_in, p.i_th, p.sigma_z);
       const double dn = zn - zt[e], di = zi - zt[e], dout = zo - zt[e];
-      if (whole || (x0 + e >= ix0 && x0 + e < ix1)) {
+      if (whole || (row_in && x0 + e >= ix0 && x0 + e < ix1)) {
         acc[0] += dn * dn;
         acc[1] += di * di + dout * dout;
         acc[2] += ((i_nom >= p.i_th) != (zt[e] != 0.0)) ? 1.0 : 0.0;
@@ -184,19 +185,20 @@ int reduce_blocks() { return kRedBlocks; }
 void launch_resist(const Grid& g, const void* If, const void* Id, const uint8_t* tu8, const double* tf,
                    ResistParams p, void* wf, void* wd, double* z_nom, double* z_in, double* z_out,
                    uint8_t* h_nom, uint8_t* h_in, uint8_t* h_out, double* partials, StopFlag stop,
-                   cudaStream_t s, int ix0, int ix1, const LoopTail* tail) {
+                   cudaStream_t s, int ix0, int ix1, const LoopTail* tail, int iy0, int iy1) {
   if (ix1 <= 0) ix1 = g.W;
+  if (iy1 > g.H) iy1 = g.H;
   const LoopTail tl = tail ? *tail : LoopTail{};
   const bool loop_form = !z_nom && !h_nom && (tu8 || tf) && partials && g.n() % 4 == 0 && g.W % 4 == 0;
   if (loop_form) {
     if (g.prec == F64)
       k_resist_loop<double><<<kRedBlocks, kRedThreads, 0, s>>>(
           g.n() / 4, static_cast<const double*>(If), static_cast<const double*>(Id), tu8, tf, p,
-          static_cast<double*>(wf), static_cast<double*>(wd), partials, stop, g.W, ix0, ix1, tl);
+          static_cast<double*>(wf), static_cast<double*>(wd), partials, stop, g.W, ix0, ix1, iy0, iy1, tl);
     else
       k_resist_loop<float><<<kRedBlocks, kRedThreads, 0, s>>>(
           g.n() / 4, static_cast<const float*>(If), static_cast<const float*>(Id), tu8, tf, p,
-          static_cast<float*>(wf), static_cast<float*>(wd), partials, stop, g.W, ix0, ix1, tl);
+          static_cast<float*>(wf), static_cast<float*>(wd), partials, stop, g.W, ix0, ix1, iy0, iy1, tl);
     return;
   }
   if (tail) throw std::invalid_argument("fused loop control needs the DSO loop form of the resist pass");
@@ -204,12 +206,12 @@ void launch_resist(const Grid& g, const void* If, const void* Id, const uint8_t*
     k_resist<double><<<kRedBlocks, kRedThreads, 0, s>>>(
         g.n(), static_cast<const double*>(If), static_cast<const double*>(Id), tu8, tf, p,
         static_cast<double*>(wf), static_cast<double*>(wd), z_nom, z_in, z_out, h_nom, h_in, h_out, partials, stop,
-        g.W, ix0, ix1);
+        g.W, ix0, ix1, iy0, iy1);
   else
     k_resist<float><<<kRedBlocks, kRedThreads, 0, s>>>(
         g.n(), static_cast<const float*>(If), static_cast<const float*>(Id), tu8, tf, p,
         static_cast<float*>(wf), static_cast<float*>(wd), z_nom, z_in, z_out, h_nom, h_in, h_out, partials, stop,
-        g.W, ix0, ix1);
+        g.W, ix0, ix1, iy0, iy1);
 }
 
 void launch_scale_intensity(const Grid& g, const void* I, double dose, double* out, cudaStream_t s) {

@@ -11,7 +11,8 @@ extern template void f2_impl<float>(const Grid& g, const SpecSet* sets, int nset
 extern template void a1_impl<float>(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
 extern template void a2_impl<float>(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
 extern template int finish_impl<float>(const Grid& g, const void* V0, const void* V1, double scale, double* out, const double* vp,
-                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1, const LoopTail* tail);
+                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1, const LoopTail* tail, int iy0,
+                int iy1);
 extern template void mask_fft_impl<double>(const Grid& g, const void* src, int kind, void* mhat, void* scratch, StopFlag stop,
                    cudaStream_t s);
 extern template void f1_impl<double>(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
@@ -19,7 +20,8 @@ extern template void f2_impl<double>(const Grid& g, const SpecSet* sets, int nse
 extern template void a1_impl<double>(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
 extern template void a2_impl<double>(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
 extern template int finish_impl<double>(const Grid& g, const void* V0, const void* V1, double scale, double* out, const double* vp,
-                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1, const LoopTail* tail);
+                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1, const LoopTail* tail, int iy0,
+                int iy1);
 }  // namespace spec
 
 using namespace spec;
@@ -76,9 +78,9 @@ void launch_adjoint(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop
 
 int launch_adjoint_finish(const Grid& g, const void* V0, const void* V1, double scale, double* out,
                           const double* vp, double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1,
-                          const LoopTail* tail) {
-  if (g.prec == F64) return finish_impl<double>(g, V0, V1, scale, out, vp, dots, stop, s, ix0, ix1, tail);
-  return finish_impl<float>(g, V0, V1, scale, out, vp, dots, stop, s, ix0, ix1, tail);
+                          const LoopTail* tail, int iy0, int iy1) {
+  if (g.prec == F64) return finish_impl<double>(g, V0, V1, scale, out, vp, dots, stop, s, ix0, ix1, tail, iy0, iy1);
+  return finish_impl<float>(g, V0, V1, scale, out, vp, dots, stop, s, ix0, ix1, tail, iy0, iy1);
 }
 
 // K0: spectra, row pass then column pass, stored column-tiled in the plan's

@@ -617,7 +617,8 @@ template <typename R> struct A3Op : OpBase {
   double* out;
   const double* vp;
   double* dots;
-  int ix0, ix1;  // dots over columns [ix0, ix1)
+  int ix0, ix1;  // dots over columns [ix0, ix1) ...
+  int iy0, iy1;  // ... and rows [iy0, iy1)
   LS_D void prefetch(int it, int, C* b, C*) const {
     eng::gather_rect<sizeof(C)>(b, V0, sh.rm(), it << sh.lgR, sh.lgR, 0, sh.lgW);
   }
@@ -629,7 +630,7 @@ template <typename R> struct A3Op : OpBase {
     double* out;
     const double* vp;
     State& S;
-    int y0, lgn, W, ix0, ix1;
+    int y0, lgn, W, ix0, ix1, iy0, iy1;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const C x = b[nat_row<LGN, ST>(seq, j, r, lgn)];
       if constexpr (LGN > 0) return v1 ? x + __ldg(&v1[rm_row<LGN, ST>(W, y0 + seq, j, r)]) : x;
@@ -640,7 +641,7 @@ template <typename R> struct A3Op : OpBase {
       const double val = scale * (double)v.x;
       out[p] = val;
       const int x = j + r * ST;
-      if (vp && x >= ix0 && x < ix1) {
+      if (vp && x >= ix0 && x < ix1 && y0 + seq >= iy0 && y0 + seq < iy1) {
         const double q = vp[p];
         S.acc[0] += val * (val - q);
         S.acc[1] += q * q;
@@ -651,7 +652,7 @@ template <typename R> struct A3Op : OpBase {
     const Geo g = sh.grow();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      F<LGN> f{b, V1, sh.rm(), scale, out, vp, S, it << sh.lgR, sh.lgW, sh.W, ix0, ix1};
+      F<LGN> f{b, V1, sh.rm(), scale, out, vp, S, it << sh.lgR, sh.lgW, sh.W, ix0, ix1, iy0, iy1};
       eng::run_fix<LGN, false, true>(g, b, tw, f);
     });
   }
@@ -1970,7 +1971,8 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
 
 template <typename R>
 int finish_impl(const Grid& g, const void* V0, const void* V1, double scale, double* out, const double* vp,
-                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1, const LoopTail* tail) {
+                double* dots, StopFlag stop, cudaStream_t s, int ix0, int ix1, const LoopTail* tail, int iy0,
+                int iy1) {
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   A3Op<R> a3;
@@ -1984,6 +1986,8 @@ int finish_impl(const Grid& g, const void* V0, const void* V1, double scale, dou
   a3.dots = dots;
   a3.ix0 = ix0;
   a3.ix1 = ix1 > 0 ? ix1 : g.W;
+  a3.iy0 = iy0;
+  a3.iy1 = iy1 < g.H ? iy1 : g.H;
   a3.tail = tail && vp ? *tail : LoopTail{};
   a3.bufE = row_bufE(sh);
   a3.nitems = g.H >> sh.lgR;

@@ -52,30 +52,39 @@ def test_strip_geometry():
         tiled.strip_geometry(64, 100, 3, 0, 35)
     with pytest.raises(ValueError):
         tiled.strip_geometry(64, 128, 2, 0, 35)
+    # row strips: the same geometry in the transposed frame
+    r = tiled.strip_geometry(8192, 8192, 8, 3, 35, axis=0)
+    assert (r.ww, r.hl, r.interior, r.window_shape) == (2048, 512, (512, 1536), (2048, 8192))
+    assert tiled.strip_geometry(1024, 64, 4, 0, 35, axis=0).stencil_bounds() == (128, 512)
 
 
-def _halo_worker(rank, world, port, q, W, K, tags):
+def _halo_worker(rank, world, port, q, W, K, tags, axis=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        s = tiled.strip_geometry(8, W, world, rank, K)
+        s = tiled.strip_geometry(8, W, world, rank, K) if axis == 1 else tiled.strip_geometry(W, 8, world, rank, K, 0)
         phi = torch.full((8, s.ww), -1.0, dtype=torch.float64)
         i0, i1 = s.interior
         phi[:, i0:i1] = torch.as_tensor(s.columns()[i0:i1], dtype=torch.float64)
+        if axis == 0:  # row strips: the window is (ww x 8), lines are rows
+            phi = phi.t().contiguous()
         tiled.exchange_halos(phi, s, tags=tags)
+        if axis == 0:
+            phi = phi.t().contiguous()
         q.put((rank, phi.numpy(), s.columns(), s.interior, s.halo))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("axis", [1, 0])
 @pytest.mark.parametrize("tags", [True, False])
 @pytest.mark.parametrize("world", [2, 4])
-def test_halo_exchange_gloo(world, tags):
+def test_halo_exchange_gloo(world, tags, axis):
     """tags=False: every message carries the same tag, so the two messages
     between the ranks of a world-2 ring are matched by position only -- the
-    way NCCL matches them (it ignores P2P tags)."""
+    way NCCL matches them (it ignores P2P tags).  axis 0: row strips."""
     W, K = 1024, 35
-    for rank, phi, cols, (i0, i1), h in _run(world, _halo_worker, W, K, tags):
+    for rank, phi, cols, (i0, i1), h in _run(world, _halo_worker, W, K, tags, axis):
         # interior and HALO columns on each side hold the global column index (wrapping)
         assert np.array_equal(phi[:, i0 - h:i1 + h], np.broadcast_to(cols[i0 - h:i1 + h], (8, i1 - i0 + 2 * h)))
 
@@ -98,7 +107,7 @@ def _ks(arrs, cond):
     return b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(*arrs)], cond)
 
 
-def _tiled_worker(rank, world, port, q, max_iters):
+def _tiled_worker(rank, world, port, q, max_iters, axis=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
@@ -109,7 +118,7 @@ def _tiled_worker(rank, world, port, q, max_iters):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         t, f, d = _case()
-        r = tiled.optimize_tiled(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=max_iters))
+        r = tiled.optimize_tiled(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=max_iters), axis=axis)
         h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
         q.put((rank, h, r.final_mask, r.metrics.l2, r.metrics.pvband))
     finally:
@@ -127,12 +136,13 @@ def _reference(max_iters):
 
 
 @pytest.mark.gpu
-def test_single_strip_is_bit_identical_to_optimize():
+@pytest.mark.parametrize("axis", [0, 1])
+def test_single_strip_is_bit_identical_to_optimize(axis):
     import paper_2303_12529_b200 as b2
     from paper_2303_12529_b200 import _native as nv
     nv.set_precision("fp64")
     t, f, d = _case()
-    r = tiled.optimize_tiled(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=12))
+    r = tiled.optimize_tiled(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=12), axis=axis)
     h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
     hr, mr, l2, pvb = _reference(12)
     assert np.array_equal(h, hr)
@@ -140,12 +150,14 @@ def test_single_strip_is_bit_identical_to_optimize():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("axis", [0, 1])
 @pytest.mark.parametrize("world", [2, 4])
-def test_strips_match_single_tile(world):
+def test_strips_match_single_tile(world, axis):
     """Ranks share cuda:0 over gloo; interior results equal the full-tile run
-    up to summation order of the global reductions."""
+    up to summation order of the global reductions; row (axis 0) and column
+    (axis 1) strips."""
     hr, mr, l2, pvb = _reference(12)
-    for rank, h, mask, l2r, pvbr in _run(world, _tiled_worker, 12, timeout=600):
+    for rank, h, mask, l2r, pvbr in _run(world, _tiled_worker, 12, axis, timeout=600):
         assert h.shape == hr.shape
         assert np.allclose(h, hr, rtol=1e-9, atol=1e-12)
         assert np.array_equal(mask, mr)
