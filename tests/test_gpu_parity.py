@@ -632,3 +632,22 @@ def test_optimize_target_dtypes_binarised():
         assert (r.metrics.l2, r.metrics.pvband) == (ref.metrics.l2, ref.metrics.pvband)
     with pytest.raises(b2.DegenerateInputError):
         b2.optimize(np.full((32, 32), 5, dtype=np.uint8), F, D, b2.OptConfig(max_iters=2))
+
+
+@pytest.mark.parametrize("prec_name", ["fp64", "fp32"])
+def test_stacked_ffts_match_reference(prec_name):
+    """KernelSet.stacked_ffts (the device K0 build, downloaded) against the
+    reference's own (Hf, Hrot_f, sigma) (litho.py:71-82; golden from
+    tests/golden/make_spectra.py)."""
+    nv.set_precision(prec_name)
+    g = golden("spectra")
+    tol = 1e-12 if prec_name == "fp64" else 2e-7
+    for side, n_k, seed, shape in [(9, 2, 3, (32, 48)), (17, 4, 1, (64, 64)), (7, 2, 0, (16, 128))]:
+        f, d, F, D = kernels(side, n_k, seed)
+        for tag, ks in (("f", F), ("d", D)):
+            key = f"{side}_{n_k}_{seed}_{tag}_{shape[0]}x{shape[1]}"
+            hf, hrot, sigma = ks.stacked_ffts(shape)
+            scale = np.abs(g[key + "_hf"]).max()
+            assert np.abs(hf - g[key + "_hf"]).max() <= tol * scale, (key, prec_name)
+            assert np.abs(hrot - g[key + "_hrot"]).max() <= tol * scale, (key, prec_name)
+            assert np.array_equal(sigma, g[key + "_sigma"])

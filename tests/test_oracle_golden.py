@@ -121,3 +121,17 @@ def test_modulation_search_matches_reference():
     r = o.modulation_search(phi, t, f, d, o.Cfg(curvature_weight=0.0), num_samples=5, eval_steps=3)
     assert np.array_equal(np.array(r["candidates"]), g["nocurvw_candidates"])
     assert r["best_delta_h"] == float(g["nocurvw_best"])
+
+
+def test_oracle_spectra_match_reference_stacked_ffts():
+    """`o.spectra` / `o.reverse_freq` against the reference's own
+    KernelSet.stacked_ffts (litho.py:71-82), tests/golden/make_spectra.py."""
+    g = golden("spectra")
+    for side, n_k, seed, shape in [(9, 2, 3, (32, 48)), (17, 4, 1, (64, 64)), (7, 2, 0, (16, 128))]:
+        f, d = o.synthetic_kernels(side, n_k, seed)
+        for tag, (c, w) in (("f", f), ("d", d)):
+            key = f"{side}_{n_k}_{seed}_{tag}_{shape[0]}x{shape[1]}"
+            hf = o.spectra(c, shape)
+            assert np.abs(hf - g[key + "_hf"]).max() <= 1e-12 * np.abs(g[key + "_hf"]).max()
+            assert np.abs(o.reverse_freq(hf) - g[key + "_hrot"]).max() <= 1e-12 * np.abs(g[key + "_hf"]).max()
+            assert np.array_equal(w, g[key + "_sigma"])
