@@ -41,6 +41,11 @@ struct SpecSet {
   void* I;           // real intensity sum_k w_k |A_k|^2, row-major (element R)
   const void* gate;  // real gate, row-major (element R)
   void* V;           // complex adjoint accumulator (column-tiled)
+  // kernel groups (small grids): per-group partials of I and V, and the
+  // tickets of the last-arriving group item (null: no groups)
+  void* Ipart;       // 8 groups x 2 sets x H*W elements R
+  void* Vpart;       // 8 groups x 2 sets x H*W complex
+  unsigned* tick;    // 2 passes x 2 sets x max(H, W) tickets, zero between launches
 };
 
 // K0: spectra of nk K x K kernels (float64 transform, stored in plan precision)

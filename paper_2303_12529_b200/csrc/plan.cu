@@ -82,9 +82,11 @@ struct lsopc_plan {
   // largest (focus + defocus) kernel count used on this plan.
   // A: per-kernel row-major fields A_k (F2 -> A1).
   DevBuf tw, tw64, mhat, scratch, scratch2, T, A, V0, V1, If, Id, wf, wd, partials, scal, hard, tsdf_i, tsdf_f;
+  // small grids: kernel-group partials of I and V and their tickets (spectral.cuh choose_lgg)
+  DevBuf Ipart, Vpart, tick;
   ~lsopc_plan() {
     for (DevBuf* b : {&tw, &tw64, &mhat, &scratch, &scratch2, &T, &A, &V0, &V1, &If, &Id, &wf, &wd, &partials,
-                      &scal, &hard, &tsdf_i, &tsdf_f})
+                      &scal, &hard, &tsdf_i, &tsdf_f, &Ipart, &Vpart, &tick})
       b->release();
   }
   // bumped whenever T or A is reallocated: CUDA graphs captured before that
@@ -150,6 +152,9 @@ SpecSet spec_set(lsopc_plan* p, const lsopc_kset* ks, int which, size_t T_off_ke
   s.I = which == 0 ? p->If.p : p->Id.p;
   s.gate = which == 0 ? p->wf.p : p->wd.p;
   s.V = which == 0 ? p->V0.p : p->V1.p;
+  s.Ipart = p->Ipart.p;
+  s.Vpart = p->Vpart.p;
+  s.tick = p->tick.as<unsigned>();
   return s;
 }
 
@@ -220,6 +225,12 @@ int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
       p->wd.ensure(n * p->g.rsize());
       size_t np = (size_t)std::max(std::max(reduce_blocks(), ls_blocks()), H) * 4 + 64;
       p->partials.ensure(np * sizeof(double));
+      if (n <= ((size_t)1 << 18)) {  // few items per pass: kernel groups (<= 8) fill the SMs
+        p->Ipart.ensure(8 * 2 * n * p->g.rsize());
+        p->Vpart.ensure(8 * 2 * n * p->g.csize());
+        p->tick.ensure(4 * (size_t)std::max(H, W) * sizeof(unsigned));
+        ck(cudaMemset(p->tick.p, 0, 4 * (size_t)std::max(H, W) * sizeof(unsigned)), "memset");
+      }
       p->scal.ensure(64 * sizeof(double));
       p->hard.ensure(3 * n);
     } catch (...) {

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
 #pragma unroll
   for (int d = 0; d < NB - 1; ++d) {
 #ifndef LSB_EXP_NOGATHER  // experiment switch: never fetch operands
-    if (pit < op.nitems) op.prefetch(pit, pst, base + d * op.bufE, extra);
+    if (pit < op.nitems) op.prefetch(pit, op.kbase(pit) + pst, base + d * op.bufE, extra);
 #endif
     eng::cp_commit();
     if (pit < op.nitems) advance(pit, pst);
@@ -133,14 +133,14 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
   while (true) {
     const int pslot = slot == 0 ? NB - 1 : slot - 1;  // == (slot + NB - 1) % NB
 #ifndef LSB_EXP_NOGATHER
-    if (pit < op.nitems) op.prefetch(pit, pst, base + pslot * op.bufE, extra);
+    if (pit < op.nitems) op.prefetch(pit, op.kbase(pit) + pst, base + pslot * op.bufE, extra);
 #endif
     eng::cp_commit();
     eng::cp_wait<NB - 1>();
     __syncthreads();
     C* const cur = base + slot * op.bufE;
     if (st == 0) op.begin(S, it, extra);
-    op.step(S, it, st, cur, extra);
+    op.step(S, it, op.kbase(it) + st, cur, extra);
     __syncthreads();
     if (st == op.steps(it) - 1) op.end(S, it, cur, extra);
     if (pit < op.nitems) advance(pit, pst);
@@ -155,6 +155,13 @@ struct NoState {};
 struct OpBase {
   static constexpr int kStages = 3;
   int bufE = 0, nitems = 0;
+  // Kernel groups (small grids, too few items for the SMs): item index =
+  // ((set << lgg | group) << lgt) | block; a group item runs kernels
+  // [group * kpg, (group + 1) * kpg).  lgg = 0: one group per set.
+  int lgg = 0, kpg = 0;
+  LS_D int set_of(int it, int lgt) const { return (it >> lgt) >> lgg; }
+  LS_D int grp_of(int it, int lgt) const { return (it >> lgt) & ((1 << lgg) - 1); }
+  LS_D int kbase(int) const { return 0; }
   LS_D int steps(int) const { return 1; }
   template <class S, class C> LS_D void begin(S&, int, C*) const {}
   template <class S, class C> LS_D void end(S&, int, C*, C*) const {}
@@ -342,7 +349,35 @@ template <typename R> struct SetArgs {
   const R* gate[2];      // row-major gate per set
   C* V[2];               // column-tiled adjoint accumulator per set
   R w[2][kMaxK];         // kernel weights (sigma_k)
+  R* Ipart;              // kernel groups: per-group partial I / V, [set][group][H*W]
+  C* Vpart;
+  unsigned* tick;        // [pass (F2, A2)][set][block] last-arriving tickets
+  int tick_stride;       // tickets per (pass, set)
 };
+
+// Kernel groups: the item of the last group to finish a (set, block) sums the
+// groups' partials in group order (deterministic whatever the arrival order)
+// into the set's output and re-arms the ticket.  Called by every thread.
+template <typename T>
+LS_D void group_combine(const T* part, size_t pstride, T* out, size_t off, int rows, int width, int ld, int G,
+                        unsigned* ticket) {
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == (unsigned)(G - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int cnt = rows * width;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const size_t p = off + (size_t)(i / width) * ld + (i % width);
+    T acc = __ldcg(&part[p]);
+    for (int g = 1; g < G; ++g) acc = acc + __ldcg(&part[(size_t)g * pstride + p]);
+    out[p] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ticket = 0;
+}
 
 // F1: T_k = IFFT_y(M^ . H_k) / (HW); the item's M^ values stay in registers
 template <typename R> struct F1Op : OpBase {
@@ -355,11 +390,12 @@ template <typename R> struct F1Op : OpBase {
   R scale;
   const C* tw;
   int lgnt;
-  LS_D int steps(int it) const { return a.nk[it >> lgnt]; }
+  LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnt)]; }
+  LS_D int kbase(int it) const { return grp_of(it, lgnt) * kpg; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
-  LS_D const C* field(int it, int k) const { return a.spec[it >> lgnt] + (size_t)k * fsz(); }  // column-tiled input
+  LS_D const C* field(int it, int k) const { return a.spec[set_of(it, lgnt)] + (size_t)k * fsz(); }  // column-tiled input
   LS_D void prefetch(int it, int k, C* b, C*) const {
-    const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
+    const int set = set_of(it, lgnt), t = it & ((1 << lgnt) - 1);
     eng::gather_rect<sizeof(C)>(b, a.spec[set] + (size_t)k * fsz(), sh.ct(), 0, sh.lgH, t << sh.lgS, sh.lgS);
   }
   // the item's M^ values, pre-multiplied by the IFFT's 1/(HW) (a power of
@@ -399,7 +435,7 @@ template <typename R> struct F1Op : OpBase {
     }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
-    const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
+    const int set = set_of(it, lgnt), t = it & ((1 << lgnt) - 1);
     const Geo g = sh.gcol();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -419,10 +455,11 @@ template <typename R> struct F2Op : OpBase {
   SetArgs<R> a;
   const C* tw;
   int lgnb;
-  LS_D int steps(int it) const { return a.nk[it >> lgnb]; }
+  LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnb)]; }
+  LS_D int kbase(int it) const { return grp_of(it, lgnb) * kpg; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
   LS_D void prefetch(int it, int k, C* b, C*) const {
-    const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
+    const int set = set_of(it, lgnb), yb = it & ((1 << lgnb) - 1);
     eng::gather_rect<sizeof(C)>(b, a.T[set] + (size_t)k * fsz(), sh.ctT(), yb << sh.lgR, sh.lgR, 0, sh.lgW);
   }
   LS_D void begin(State& S, int, C*) const {
@@ -442,7 +479,7 @@ template <typename R> struct F2Op : OpBase {
     }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
-    const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
+    const int set = set_of(it, lgnb), yb = it & ((1 << lgnb) - 1);
     const Geo g = sh.grow();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -459,7 +496,7 @@ template <typename R> struct F2Op : OpBase {
     }
   };
   LS_D void end(State& S, int it, C*, C*) const {
-    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     const Geo g = sh.grow();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -478,10 +515,11 @@ template <typename R> struct A1Op : OpBase {
   SetArgs<R> a;
   const C* tw;
   int lgnb;
-  LS_D int steps(int it) const { return a.nk[it >> lgnb]; }
+  LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnb)]; }
+  LS_D int kbase(int it) const { return grp_of(it, lgnb) * kpg; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
   LS_D void prefetch(int it, int k, C* b, C*) const {
-    const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
+    const int set = set_of(it, lgnb), yb = it & ((1 << lgnb) - 1);
     eng::gather_rect<sizeof(C)>(b, a.A[set] + (size_t)k * fsz(), sh.rm(), yb << sh.lgR, sh.lgR, 0, sh.lgW);
   }
   template <int LGN> struct LoadG {
@@ -493,7 +531,7 @@ template <typename R> struct A1Op : OpBase {
     }
   };
   LS_D void begin(State& S, int it, C*) const {
-    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     eng::dispatch<C>(sh.grow(), sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       if constexpr (LGN > 0) eng::for_first_slots<LGN, false, C>(LoadG<LGN>{S, a.gate[set], y0, sh.W});
@@ -514,7 +552,7 @@ template <typename R> struct A1Op : OpBase {
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { gstore(out[ct_row<LGN, ST, C>(L, y0 + seq, j, r)], v); }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
-    const int set = it >> lgnb, yb = it & ((1 << lgnb) - 1);
+    const int set = set_of(it, lgnb), yb = it & ((1 << lgnb) - 1);
     const Geo g = sh.grow();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -533,11 +571,12 @@ template <typename R> struct A2Op : OpBase {
   SetArgs<R> a;
   const C* tw;
   int lgnt;
-  LS_D int steps(int it) const { return a.nk[it >> lgnt]; }
+  LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnt)]; }
+  LS_D int kbase(int it) const { return grp_of(it, lgnt) * kpg; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
-  LS_D const C* field(int it, int k) const { return a.T[it >> lgnt] + (size_t)k * fsz(); }  // column-tiled U_k
+  LS_D const C* field(int it, int k) const { return a.T[set_of(it, lgnt)] + (size_t)k * fsz(); }  // column-tiled U_k
   LS_D void prefetch(int it, int k, C* b, C*) const {
-    const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
+    const int set = set_of(it, lgnt), t = it & ((1 << lgnt) - 1);
     eng::gather_rect<sizeof(C)>(b, a.T[set] + (size_t)k * fsz(), sh.ct(), 0, sh.lgH, t << sh.lgS, sh.lgS);
   }
   LS_D void begin(State& S, int, C*) const {
@@ -563,7 +602,7 @@ template <typename R> struct A2Op : OpBase {
     template <int ST> LS_D void store(int, int, int, C v, int slot) { S.acc[slot] = S.acc[slot] + cmulc(v, h[slot]) * w; }
   };
   LS_D void step(State& S, int it, int k, C* b, C*) const {
-    const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
+    const int set = set_of(it, lgnt), t = it & ((1 << lgnt) - 1);
     const Geo g = sh.gcol();
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -592,16 +631,21 @@ template <typename R> struct A2Op : OpBase {
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[rm_col<LGN, ST>(W, j, r, x0 + seq)] = v; }
   };
   LS_D void end(State& S, int it, C* b, C*) const {
-    const int set = it >> lgnt, t = it & ((1 << lgnt) - 1);
+    const int set = set_of(it, lgnt), t = it & ((1 << lgnt) - 1);
     const Geo g = sh.gcol();
+    const size_t n = (size_t)sh.H * sh.W;
+    C* dst = lgg ? a.Vpart + (size_t)((set << lgg) + grp_of(it, lgnt)) * n : a.V[set];
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       eng::for_last_slots<LGN, true, C>(g, PutAcc<LGN>{b, S, sh.lgS});
       __syncthreads();
-      FOut<LGN> f{b, a.V[set], sh.W, t << sh.lgS, sh.lgS};
+      FOut<LGN> f{b, dst, sh.W, t << sh.lgS, sh.lgS};
       eng::run_fix<LGN, true, true>(g, b, tw, f);
     });
     __syncthreads();
+    if (lgg)  // the IFFT is linear: the groups' transformed partials sum to V
+      group_combine(a.Vpart + (size_t)(set << lgg) * n, n, a.V[set], (size_t)(t << sh.lgS), sh.H, 1 << sh.lgS, sh.W,
+                    1 << lgg, &a.tick[(2 + set) * a.tick_stride + t]);
   }
 };
 
@@ -779,7 +823,7 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
     tma::mbar_expect_tx(&bar[0], 0);
 #else
     tma::mbar_expect_tx(&bar[0], op.load_bytes());
-    op.load(nit, nst, base, &bar[0]);
+    op.load(nit, op.kbase(nit) + nst, base, &bar[0]);
 #endif
   }
   advance(nit, nst);
@@ -798,7 +842,7 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
       tma::mbar_expect_tx(&bar[nslot], 0);
 #else
       tma::mbar_expect_tx(&bar[nslot], op.load_bytes());
-      op.load(nit, nst, base + nslot * op.bufE, &bar[nslot]);
+      op.load(nit, op.kbase(nit) + nst, base + nslot * op.bufE, &bar[nslot]);
 #endif
     }
     if constexpr (Op::kSideLoad) {
@@ -807,7 +851,7 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
         tma::mbar_expect_tx(&bar[3 + (q & 1)], 0);
 #else
         tma::mbar_expect_tx(&bar[3 + (q & 1)], op.load_bytes());
-        op.side_load(it, st, side, &bar[3 + (q & 1)]);
+        op.side_load(it, op.kbase(it) + st, side, &bar[3 + (q & 1)]);
 #endif
       }
     }
@@ -816,17 +860,17 @@ __global__ void __launch_bounds__(eng::cta_threads<typename CT<R>::C>(), 1) k_pa
     if (st == 0) op.begin(S, it, cur);
     if constexpr (Op::kSideLoad) {
       const bool item_end = st == op.steps(it) - 1;
-      op.step_side(S, it, st, cur, side, q, bar, !item_end);
+      op.step_side(S, it, op.kbase(it) + st, cur, side, q, bar, !item_end);
       side_pending = item_end;
     } else {
-      op.step(S, it, st, cur, side, q);
+      op.step(S, it, op.kbase(it) + st, cur, side, q);
     }
     if (Op::kStores) {
       tma::fence_async_smem();
       __syncthreads();
       if (leader) {
 #ifndef LSB_EXP_NOTMA
-        op.store(it, st, cur);
+        op.store(it, op.kbase(it) + st, cur);
 #endif
         tma::bulk_commit();
       }
@@ -1105,10 +1149,11 @@ template <typename R> struct TF1Op : OpBase {
   alignas(64) CUtensorMap tmap_spec1;  // spectra of set 1
   alignas(64) CUtensorMap tmap_T;     // T fields, column-item boxes
   int koff[2];                      // first kernel index of each set in the stacked maps
-  LS_D int steps(int it) const { return a.nk[it >> lgnt]; }
+  LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnt)]; }
+  LS_D int kbase(int it) const { return grp_of(it, lgnt) * kpg; }
   LS_D unsigned load_bytes() const { return (unsigned)((sh.H << sh.lgS) * sizeof(C)); }
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
-    const int set = it >> lgnt, x0 = (it & ((1 << lgnt) - 1)) << sh.lgS;
+    const int set = set_of(it, lgnt), x0 = (it & ((1 << lgnt) - 1)) << sh.lgS;
     if (spec_lgw == sh.lgS) {  // the item is one whole tile: a contiguous block, one 1-D bulk copy
       tma::bulk_g2s(dst, a.spec[set] + (size_t)k * sh.H * sh.W + ((size_t)(x0 >> spec_lgw) * sh.H << spec_lgw),
                     load_bytes(), bar);
@@ -1120,7 +1165,7 @@ template <typename R> struct TF1Op : OpBase {
     });
   }
   LS_D void store(int it, int k, const C* src) const {
-    const int set = it >> lgnt, x0 = (it & ((1 << lgnt) - 1)) << sh.lgS;
+    const int set = set_of(it, lgnt), x0 = (it & ((1 << lgnt) - 1)) << sh.lgS;
     col_boxes(x0, k + koff[set], kLgTileT, [&](int c0, int c1, int c2, int kk, int off) {
       tma::tensor_s2g(&tmap_T, c0, c1, c2, kk, src + off);
     });
@@ -1174,11 +1219,12 @@ template <typename R> struct TF2Op : OpBase {
   int split_lgq;                   // >= 0: T rows stored in split order (split_row)
   alignas(64) CUtensorMap tmap_T;  // T fields, row-item boxes
   int koff[2];
-  LS_D int steps(int it) const { return a.nk[it >> lgnb]; }
+  LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnb)]; }
+  LS_D int kbase(int it) const { return grp_of(it, lgnb) * kpg; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
   LS_D unsigned load_bytes() const { return (unsigned)((sh.W << sh.lgR) * sizeof(C)); }
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
-    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     const int tiles = sh.W >> kLgTileT, bt = tiles < 256 ? tiles : 256;
     for (int r = 0; r < (1 << sh.lgR); ++r) {
       const int yr = split_lgq >= 0 ? split_row(y0 + r, split_lgq) : y0 + r;
@@ -1187,7 +1233,7 @@ template <typename R> struct TF2Op : OpBase {
     }
   }
   LS_D void store(int it, int k, const C* src) const {
-    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     tma::bulk_s2g(a.A[set] + (size_t)k * fsz() + ((size_t)y0 << sh.lgW), src, load_bytes());
   }
   LS_D void begin(State& S, int, C*) const {
@@ -1209,18 +1255,23 @@ template <typename R> struct TF2Op : OpBase {
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       if constexpr (LGN > 0) {
-        F<LGN> f{b, S, a.w[it >> lgnb][k]};
+        F<LGN> f{b, S, a.w[set_of(it, lgnb)][k]};
         eng::run_fix<LGN, false, true>(g, b, tw, f);
       }
     });
   }
   LS_D void end(State& S, int it, C*, C*) const {
-    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int set = set_of(it, lgnb), blk = it & ((1 << lgnb) - 1), y0 = blk << sh.lgR;
     const Geo g = sh.grow();
+    const size_t n = (size_t)sh.H * sh.W;
+    R* dst = lgg ? a.Ipart + (size_t)((set << lgg) + grp_of(it, lgnb)) * n : a.I[set];
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      eng::for_last_slots<LGN, false, C>(g, typename F2Op<R>::template WriteI<LGN>{a.I[set], S, y0, sh.W});
+      eng::for_last_slots<LGN, false, C>(g, typename F2Op<R>::template WriteI<LGN>{dst, S, y0, sh.W});
     });
+    if (lgg)
+      group_combine(a.Ipart + (size_t)(set << lgg) * n, n, a.I[set], (size_t)y0 * sh.W, 1 << sh.lgR, sh.W, sh.W,
+                    1 << lgg, &a.tick[set * a.tick_stride + blk]);
   }
 };
 
@@ -1237,15 +1288,16 @@ template <typename R> struct TA1Op : OpBase {
   int lgnb;
   alignas(64) CUtensorMap tmap_U;  // U fields (layout tile lg_tile<C>), row-item boxes
   int koff[2];
-  LS_D int steps(int it) const { return a.nk[it >> lgnb]; }
+  LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnb)]; }
+  LS_D int kbase(int it) const { return grp_of(it, lgnb) * kpg; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
   LS_D unsigned load_bytes() const { return (unsigned)((sh.W << sh.lgR) * sizeof(C)); }
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
-    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     tma::bulk_g2s(dst, a.A[set] + (size_t)k * fsz() + ((size_t)y0 << sh.lgW), load_bytes(), bar);
   }
   LS_D void store(int it, int k, const C* src) const {
-    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     constexpr int LGT = lg_tile<C>();
     const int tiles = sh.W >> LGT, bt = tiles < 256 ? tiles : 256;
     for (int r = 0; r < (1 << sh.lgR); ++r)
@@ -1253,7 +1305,7 @@ template <typename R> struct TA1Op : OpBase {
         tma::tensor_s2g(&tmap_U, 0, b * bt, y0 + r, k + koff[set], src + (r << sh.lgW) + ((b * bt) << LGT));
   }
   LS_D void begin(State& S, int it, C*) const {
-    const int set = it >> lgnb, y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
+    const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     eng::dispatch<C>(sh.grow(), true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       if constexpr (LGN > 0)
@@ -1305,7 +1357,7 @@ template <typename R> struct TA2Op : A2Op<R> {
   // whole-tile items are contiguous blocks: one 1-D bulk copy each
   LS_D size_t tile_off(int x0) const { return (size_t)(x0 >> u_lgw) * this->sh.H << u_lgw; }
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
-    const int set = it >> this->lgnt, x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
+    const int set = this->set_of(it, this->lgnt), x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
     if (u_lgw == this->sh.lgS) {
       tma::bulk_g2s(dst, this->a.T[0] + (size_t)(k + koff[set]) * this->sh.H * this->sh.W + tile_off(x0),
                     load_bytes(), bar);
@@ -1316,7 +1368,7 @@ template <typename R> struct TA2Op : A2Op<R> {
     });
   }
   LS_D void side_load(int it, int k, C* dst, uint64_t* bar) const {
-    const int set = it >> this->lgnt, x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
+    const int set = this->set_of(it, this->lgnt), x0 = (it & ((1 << this->lgnt) - 1)) << this->sh.lgS;
     if (u_lgw == this->sh.lgS) {
       tma::bulk_g2s(dst, this->a.spec[set] + (size_t)k * this->sh.H * this->sh.W + tile_off(x0), load_bytes(), bar);
       return;
@@ -1359,7 +1411,7 @@ template <typename R> struct TA2Op : A2Op<R> {
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       if constexpr (LGN > 0) {
-        F<LGN> f{b, side, &bars[3 + (q & 1u)], (q >> 1) & 1u, S, this->a.w[it >> this->lgnt][k],
+        F<LGN> f{b, side, &bars[3 + (q & 1u)], (q >> 1) & 1u, S, this->a.w[this->set_of(it, this->lgnt)][k],
                  this, it, k + 1, &bars[3 + ((q + 1) & 1u)], issue_next};
         eng::run_fix<LGN, true, false>(g, b, this->tw, f);
       }
@@ -1369,6 +1421,14 @@ template <typename R> struct TA2Op : A2Op<R> {
 
 // ---------------------------------------------------------------------------
 // launch plumbing
+
+// the dynamic shared-memory allowance left beside a kernel's static shared
+// memory (the kernel-group combine keeps a flag there), out of 227 KB
+template <class K> int max_dyn_smem(K* kern) {
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, kern);
+  return 227 * 1024 - (int)fa.sharedSizeBytes;
+}
 
 inline int num_sms() {
   static int n = 0;
@@ -1392,7 +1452,7 @@ int launch_op(Op& op, int threads, int extra_bufs, StopFlag stop, cudaStream_t s
   static size_t per_sm_smem = 0;
   static int per_sm_threads = 0;
   if (per_sm < 0 || per_sm_smem != smem || per_sm_threads != threads) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem(kern));
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem);
@@ -1415,7 +1475,7 @@ int launch_tma(Op& op, int threads, StopFlag stop, cudaStream_t s) {
   auto kern = k_pass_tma<R, Op>;
   static int per_sm = -1;
   if (per_sm < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem(kern));
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem);
@@ -1654,7 +1714,7 @@ void launch_cluster(Op& op, int ntiles, int nsets, StopFlag stop, cudaStream_t s
   static int fit = 0;
   static size_t fit_smem = 0;
   if (!fit || fit_smem != smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem(kern));
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sms() / kClusterCols * kClusterCols);
@@ -1732,7 +1792,27 @@ template <typename R> SetArgs<R> set_args(const Grid& g, const SpecSet* sets, in
     a.V[i] = static_cast<C*>(sets[i].V);
     for (int k = 0; k < sets[i].nk; ++k) a.w[i][k] = (R)sets[i].w[k];
   }
+  a.Ipart = static_cast<R*>(sets[0].Ipart);
+  a.Vpart = static_cast<C*>(sets[0].Vpart);
+  a.tick = sets[0].tick;
+  a.tick_stride = std::max(g.H, g.W);
   return a;
+}
+
+// Kernel groups for a pass with base_items (block x set) items: the largest
+// power of two G <= 8 that keeps G * base_items within the SM count and
+// divides every set's kernel count (sets of equal size), when the plan
+// provides the partial buffers.  Returns log2 G.
+template <typename R> int choose_lgg(int base_items, const SetArgs<R>& a) {
+  if (!a.Ipart || !a.Vpart || !a.tick) return 0;
+  if (a.nsets > 1 && a.nk[0] != a.nk[1]) return 0;
+  int lgg = 0;
+  while (lgg < 3) {
+    const int G = 2 << lgg;
+    if ((long)base_items * G > (long)num_sms() || a.nk[0] % G) break;
+    ++lgg;
+  }
+  return lgg;
 }
 
 // ---------------------------------------------------------------------------
@@ -1818,7 +1898,9 @@ void f1_impl(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, St
     f1.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), cbT.first, cbT.second, rows);
     for (int i = 0; i < 2; ++i) f1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     f1.bufE = tma_bufE<R>(col_bufE(sh));
-    f1.nitems = (1 << f1.lgnt) * nsets;
+    f1.lgg = choose_lgg<R>((1 << f1.lgnt) * nsets, a);
+    f1.kpg = a.nk[0] >> f1.lgg;
+    f1.nitems = ((1 << f1.lgnt) * nsets) << f1.lgg;
     launch_tma<R>(f1, col_threads(sh), stop, s);
     return;
   }
@@ -1881,7 +1963,9 @@ void f2_impl(const Grid& g, const SpecSet* sets, int nsets, double2* a0_out, Sto
                                (unsigned)std::min(tiles, 256), 1);
     for (int i = 0; i < 2; ++i) f2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     f2.bufE = tma_bufE<R>(row_bufE(sh));
-    f2.nitems = (1 << f2.lgnb) * nsets;
+    f2.lgg = choose_lgg<R>((1 << f2.lgnb) * nsets, a);
+    f2.kpg = a.nk[0] >> f2.lgg;
+    f2.nitems = ((1 << f2.lgnb) * nsets) << f2.lgg;
     launch_tma<R>(f2, row_threads(sh), stop, s);
   } else {
     F2Op<R> f2;
@@ -1913,7 +1997,9 @@ void a1_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
                                (unsigned)std::min(tiles, 256), 1);
     for (int i = 0; i < 2; ++i) a1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     a1.bufE = tma_bufE<R>(row_bufE(sh));
-    a1.nitems = (1 << a1.lgnb) * nsets;
+    a1.lgg = choose_lgg<R>((1 << a1.lgnb) * nsets, a);
+    a1.kpg = a.nk[0] >> a1.lgg;
+    a1.nitems = ((1 << a1.lgnb) * nsets) << a1.lgg;
     launch_tma<R>(a1, row_threads(sh), stop, s);
     return;
   }
@@ -1950,7 +2036,9 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
     }
     for (int i = 0; i < 2; ++i) a2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     a2.bufE = tma_bufE<R>(col_bufE(sh));
-    a2.nitems = (1 << a2.lgnt) * nsets;
+    a2.lgg = choose_lgg<R>((1 << a2.lgnt) * nsets, a);
+    a2.kpg = a.nk[0] >> a2.lgg;
+    a2.nitems = ((1 << a2.lgnt) * nsets) << a2.lgg;
     launch_tma<R>(a2, col_threads(sh), stop, s);
     return;
   }

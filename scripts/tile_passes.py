@@ -18,9 +18,11 @@ nv.set_precision("fp32")
 focus, defocus = b2.gen_synthetic_kernels(35, 24, seed=4)
 args = [int(a) for a in sys.argv[1:]] or [8192, 2048, 2048, 8192]
 for H, W in zip(args[::2], args[1::2]):
-    t = np.zeros((H, W), dtype=np.uint8)
     big = inputs.mosaic_tile(range(16), grid=(4, 4))
-    t[:] = big[:H, :W]
+    # small grids: the centre of the first clip (its wires lie in [512, 1536)^2)
+    y0 = 1024 - H // 2 if H <= 2048 else 0
+    x0 = 1024 - W // 2 if W <= 2048 else 0
+    t = np.ascontiguousarray(big[y0:y0 + H, x0:x0 + W])
     fk, dk = focus.device((H, W)), defocus.device((H, W))
     c = b2.optimizer._native_cfg(b2.OptConfig(max_iters=20, stop_patience=10**9))
     td = nv.to_dev(t, np.uint8)

@@ -20,7 +20,7 @@ def main():
     sys.path.insert(0, sys.argv[1] if len(sys.argv) > 1 else "/tmp/refpkg")
     from lsopc import litho
     out = {}
-    for side, n_k, seed, shape in [(9, 2, 3, (32, 48)), (17, 4, 1, (64, 64)), (7, 2, 0, (16, 128))]:
+    for side, n_k, seed, shape in [(9, 2, 3, (32, 64)), (17, 4, 1, (64, 64)), (7, 2, 0, (16, 128))]:
         f, d = litho.gen_synthetic_kernels(side, n_k, seed=seed)
         for tag, ks in (("f", f), ("d", d)):
             hf, hrot, sigma = ks.stacked_ffts(shape)

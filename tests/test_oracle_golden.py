@@ -127,7 +127,7 @@ def test_oracle_spectra_match_reference_stacked_ffts():
     """`o.spectra` / `o.reverse_freq` against the reference's own
     KernelSet.stacked_ffts (litho.py:71-82), tests/golden/make_spectra.py."""
     g = golden("spectra")
-    for side, n_k, seed, shape in [(9, 2, 3, (32, 48)), (17, 4, 1, (64, 64)), (7, 2, 0, (16, 128))]:
+    for side, n_k, seed, shape in [(9, 2, 3, (32, 64)), (17, 4, 1, (64, 64)), (7, 2, 0, (16, 128))]:
         f, d = o.synthetic_kernels(side, n_k, seed)
         for tag, (c, w) in (("f", f), ("d", d)):
             key = f"{side}_{n_k}_{seed}_{tag}_{shape[0]}x{shape[1]}"
