@@ -45,7 +45,9 @@ const char* lsopc_last_error(void);
 int lsopc_abi_version(void);
 
 /* Workspace for H x W grids (powers of two, 4..8192; fields.py:1-6 contract,
- * SPEC.md:51).  precision: transforms in complex64 (FP32) or complex128. */
+ * SPEC.md:51).  precision: transforms in complex64 (FP32) or complex128.
+ * FP64 takes sides up to 4096, plus 8192 x W with 256 <= W <= 1024 (the
+ * split plan); LSOPC_EINVAL otherwise. */
 int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out);
 int lsopc_plan_destroy(lsopc_plan* plan);
 

@@ -15,6 +15,12 @@ struct Grid {
   const void* tw;       // twiddle table exp(-2 pi i j / nmax), j < nmax, element C
   const void* tw64;     // the same table in double precision (spectra builds)
   int lgnmax;           // log2 table length
+  // Tall-grid split (H = 8192): each column's transform runs as four
+  // 2048-point transforms on the decimated "planes" (frequency row 4 f2 + c
+  // -> plane c row f2, stored at row c * 2048 + f2), the column passes on the
+  // virtual 2048 x 4W grid those planes form in memory, and the radix-4
+  // combine across the planes folded into the row passes (spectral.cuh).
+  int vsplit = 0;
   size_t n() const { return (size_t)H * W; }
   size_t csize() const { return prec == F64 ? 16 : 8; }
   size_t rsize() const { return prec == F64 ? 8 : 4; }

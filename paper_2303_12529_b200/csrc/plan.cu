@@ -183,8 +183,18 @@ int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
       throw Error(LSOPC_EINVAL, "grid " + std::to_string(W) + "x" + std::to_string(H) +
                                     " unsupported: sides must be powers of two in [4, 8192]");
     if (precision != LSOPC_FP32 && precision != LSOPC_FP64) throw Error(LSOPC_EINVAL, "bad precision");
-    if (precision == LSOPC_FP64 && (H > 4096 || W > 4096))
-      throw Error(LSOPC_EINVAL, "the FP64 tier supports sides up to 4096; use the FP32 tier for larger grids");
+    // tall-grid split: 8192-point columns as four 2048-point planes, while a
+    // row item still holds the four rows (one per plane) it combines
+    const bool tma_off = [] {
+      const char* e = std::getenv("LSOPC_B200_NO_TMA");
+      return e && e[0] == '1';
+    }();
+    const char* nv = std::getenv("LSOPC_B200_NO_VSPLIT");
+    const int row_item = precision == LSOPC_FP64 ? 4096 : 8192;  // elements per row item
+    const bool vsplit = !(nv && nv[0] == '1') && !tma_off && H == 8192 && W >= 256 && W * 4 <= row_item;
+    if (precision == LSOPC_FP64 && (W > 4096 || (H > 4096 && !vsplit)))
+      throw Error(LSOPC_EINVAL, "the FP64 tier supports sides up to 4096, and 8192 x W grids with 256 <= W <= "
+                                "1024; use the FP32 tier for larger grids");
     auto* p = new lsopc_plan();
     try {
       p->g.H = H;
@@ -192,6 +202,7 @@ int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
       p->g.lgH = ilog2(H);
       p->g.lgW = ilog2(W);
       p->g.prec = precision;
+      p->g.vsplit = vsplit ? 1 : 0;
       const int nmax = H > W ? H : W;
       p->g.lgnmax = ilog2(nmax);
       std::vector<double> t64(2 * nmax);

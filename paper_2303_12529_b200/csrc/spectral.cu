@@ -36,6 +36,42 @@ __global__ void k_embed(int K, int H, int W, const double2* __restrict__ coeffs,
   int x = ((j - K / 2) % W + W) % W;
   out[(size_t)y * W + x] = cmk((RC)coeffs[t].x, (RC)coeffs[t].y);
 }
+
+// K0 of a split plan (H = 8192): the direct separable DFT of the K x K taps in
+// float64, G(i, v) = sum_j h(i, j) e^(-2 pi i v tc_j / W), then
+// H(u, v) = sum_i G(i, v) e^(-2 pi i u tr_i / H), with tc_j = (j - K/2) mod W,
+// tr_i = (i - K/2) mod H (fields.py:61-74 embedding) -- K multiply-adds per
+// output, no 8192-point transform -- stored in the plan precision,
+// column-tiled, rows in split order (u = 4 f2 + c at row c * H/4 + f2).
+__global__ void k_dft_rows(int K, int W, int lgnmax, const double2* __restrict__ h, const double2* __restrict__ tw,
+                           double2* G) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  if (v >= W) return;
+  const int step = (1 << lgnmax) / W;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j = 0; j < K; ++j) {
+    const int tc = ((j - K / 2) % W + W) % W;
+    const double2 w = tw[(int)(((long long)v * tc) % W) * step];
+    acc = acc + cmul(h[i * K + j], w);
+  }
+  G[(size_t)i * W + v] = acc;
+}
+template <typename C>
+__global__ void k_dft_cols_split(int K, int H, int W, int lgT, int lgnmax, const double2* __restrict__ G,
+                                 const double2* __restrict__ tw, C* out) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x, u = blockIdx.y;
+  if (v >= W) return;
+  const int step = (1 << lgnmax) / H;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int i = 0; i < K; ++i) {
+    const int tr = ((i - K / 2) % H + H) % H;
+    const double2 w = tw[(int)(((long long)u * tr) % H) * step];
+    acc = acc + cmul(G[(size_t)i * W + v], w);
+  }
+  const int yd = (u & 3) * (H >> 2) + (u >> 2);
+  out[(((size_t)(v >> lgT) * H + yd) << lgT) | (v & ((1 << lgT) - 1))] = cmk((decltype(C{}.x))acc.x,
+                                                                           (decltype(C{}.x))acc.y);
+}
 }  // namespace
 
 // ============================================================================
@@ -144,20 +180,37 @@ void spectra_impl(const Grid& g, int nk, int K, const double* coeffs_dev, void* 
 
 void launch_kernel_spectra(const Grid& g, int nk, int K, const double* coeffs_dev, void* spec, void* scratch,
                            void* scratch2, cudaStream_t s) {
+  if (g.vsplit) {
+    double2* G = static_cast<double2*>(scratch);
+    const double2* tw = static_cast<const double2*>(g.tw64);
+    const int lgT = g.prec == F64 ? shape_of<double>(g).lgT : shape_of<float>(g).lgT;
+    for (int k = 0; k < nk; ++k) {
+      const double2* h = reinterpret_cast<const double2*>(coeffs_dev) + (size_t)k * K * K;
+      k_dft_rows<<<dim3((g.W + 127) / 128, K), 128, 0, s>>>(K, g.W, g.lgnmax, h, tw, G);
+      if (g.prec == F64)
+        k_dft_cols_split<double2><<<dim3((g.W + 127) / 128, g.H), 128, 0, s>>>(
+            K, g.H, g.W, lgT, g.lgnmax, G, tw, static_cast<double2*>(spec) + (size_t)k * g.n());
+      else
+        k_dft_cols_split<float2><<<dim3((g.W + 127) / 128, g.H), 128, 0, s>>>(
+            K, g.H, g.W, lgT, g.lgnmax, G, tw, static_cast<float2*>(spec) + (size_t)k * g.n());
+    }
+    return;
+  }
   if (g.prec == F32 && std::max(g.H, g.W) > 4096) spectra_impl<float>(g, nk, K, coeffs_dev, spec, scratch, scratch2, s);
   else spectra_impl<double>(g, nk, K, coeffs_dev, spec, scratch, scratch2, s);
 }
 
 // spectrum field (plan precision, column-tiled) -> complex128 row-major
 void launch_spec_to_c128(const Grid& g, const void* field, double* out, cudaStream_t s) {
+  const int lgq = g.vsplit ? g.lgH - 2 : -1;  // split plans store rows in split order
   if (g.prec == F64) {
     Lay L{g.H, shape_of<double>(g).lgT};
     k_ct_to_c128<double><<<148 * 4, 256, 0, s>>>(g.n(), L, g.W, static_cast<const double2*>(field),
-                                                   reinterpret_cast<double2*>(out));
+                                                   reinterpret_cast<double2*>(out), lgq);
   } else {
     Lay L{g.H, shape_of<float>(g).lgT};
     k_ct_to_c128<float><<<148 * 4, 256, 0, s>>>(g.n(), L, g.W, static_cast<const float2*>(field),
-                                                  reinterpret_cast<double2*>(out));
+                                                  reinterpret_cast<double2*>(out), lgq);
   }
 }
 

@@ -61,6 +61,82 @@ template <typename C> constexpr int lg_tile() { return sizeof(C) == 8 ? 2 : 1; }
 LS_HD int split_row(int y, int lgq) { return ((y & 3) << lgq) | (y >> 2); }
 constexpr int kLgTileT = 3;  // T_k: read by the F2 row pass as 256 B chunks
 
+// ---- Tall-grid split (Grid::vsplit, H = 8192 = 4 x 2048) -------------------
+// With y = n2 + 2048 m and frequency f = 4 f2 + c (n2, f2 < 2048; m, c < 4):
+//   X[4 f2 + c] = FFT_2048( z_c )[f2],  z_c[n2] = tw[c n2] sum_m (-i)^(c m) x[n2 + 2048 m]
+//   x[n2 + 2048 m] = sum_c i^(c m) conj(tw[c n2]) IFFT_2048( X[4 . + c] )[n2]
+// so the radix-4 step runs inside the row passes and every column transform
+// is a 2048-point one.  Plane c (frequency rows 4 f2 + c) is stored at rows
+// c * 2048 + f2; in a column-tiled layout of tile width w this makes the
+// spectral fields exactly the column-tiled layout of a virtual 2048 x 4W
+// grid (virtual column ((x / w) * 4 + c) * w + x mod w), so the column
+// passes run unchanged on that grid.  A split row item holds R = 4Q rows:
+// buffer row m * Q + q is natural row n2_0 + q + 2048 m, or -- before the
+// inverse / after the forward combine -- plane row c * Q + q.
+constexpr int kVsM = 2048, kLgVsM = 11;
+LS_HD int vs_row(int seq, int lgq, int n20) { return n20 + (seq & ((1 << lgq) - 1)) + ((seq >> lgq) << kLgVsM); }
+LS_HD int vs_plane_row(int seq, int lgq, int n20) {  // storage row of plane row seq = c * Q + q
+  return ((seq >> lgq) << kLgVsM) + n20 + (seq & ((1 << lgq) - 1));
+}
+template <typename C> LS_D C mul_pi(C z) { return cmk(-z.y, z.x); }  // +i z (mul_mi: -i z)
+// forward combine in place: natural rows m * Q + q -> plane rows c * Q + q
+template <typename C>
+LS_D void vs_fwd_combine(C* b, int lgW, int lgq, int n20, const C* __restrict__ tw, int tws) {
+  const int cnt = 1 << (lgq + lgW);
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int q = i >> lgW, x = i & ((1 << lgW) - 1), n2 = n20 + q;
+    C* p = b + ((size_t)q << lgW) + x;
+    const size_t st = (size_t)1 << (lgq + lgW);
+    const C y0 = p[0], y1 = p[st], y2 = p[2 * st], y3 = p[3 * st];
+    const C a0 = y0 + y2, a1 = y0 - y2, b0 = y1 + y3, b1 = y1 - y3;
+    p[0] = a0 + b0;
+    p[st] = cmul(a1 + mul_mi(b1), __ldg(&tw[n2 << tws]));
+    p[2 * st] = cmul(a0 - b0, __ldg(&tw[(2 * n2) << tws]));
+    p[3 * st] = cmul(a1 + mul_pi(b1), __ldg(&tw[(3 * n2) << tws]));
+  }
+}
+// inverse combine in place: plane rows c * Q + q (+ a second accumulator
+// read from global at its storage row) -> natural rows m * Q + q
+template <typename C>
+LS_D void vs_inv_combine(C* b, int lgW, int lgq, int n20, const C* __restrict__ tw, int tws,
+                         const C* __restrict__ add = nullptr) {
+  const int cnt = 1 << (lgq + lgW);
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int q = i >> lgW, x = i & ((1 << lgW) - 1), n2 = n20 + q;
+    C* p = b + ((size_t)q << lgW) + x;
+    const size_t st = (size_t)1 << (lgq + lgW);
+    C z0 = p[0], z1 = p[st], z2 = p[2 * st], z3 = p[3 * st];
+    if (add) {
+      const size_t W = (size_t)1 << lgW, g = (size_t)n2 * W + x, pl = (size_t)kVsM * W;
+      z0 = z0 + __ldg(&add[g]);
+      z1 = z1 + __ldg(&add[g + pl]);
+      z2 = z2 + __ldg(&add[g + 2 * pl]);
+      z3 = z3 + __ldg(&add[g + 3 * pl]);
+    }
+    z1 = cmulc(z1, __ldg(&tw[n2 << tws]));
+    z2 = cmulc(z2, __ldg(&tw[(2 * n2) << tws]));
+    z3 = cmulc(z3, __ldg(&tw[(3 * n2) << tws]));
+    const C a0 = z0 + z2, a1 = z0 - z2, b0 = z1 + z3, b1 = z1 - z3;
+    p[0] = a0 + b0;
+    p[st] = a1 + mul_pi(b1);
+    p[2 * st] = a0 - b0;
+    p[3 * st] = a1 + mul_mi(b1);
+  }
+}
+// the virtual grid of a split plan's column passes
+inline Grid vs_grid(const Grid& g) {
+  Grid v = g;
+  v.H = kVsM;
+  v.lgH = kLgVsM;
+  v.W = g.W * 4;
+  v.lgW = g.lgW + 2;
+  v.vsplit = 0;
+  return v;
+}
+// virtual column xv of a tile-width-2^lgt layout -> (physical column, plane)
+LS_HD int vs_col(int xv, int lgt) { return ((xv >> (lgt + 2)) << lgt) | (xv & ((1 << lgt) - 1)); }
+LS_HD int vs_plane(int xv, int lgt) { return (xv >> lgt) & 3; }
+
 template <typename R> struct Shape {
   int H, W, lgH, lgW;
   int lgS, lgR;     // log2 columns per column item / rows per row item
@@ -91,10 +167,11 @@ template <typename R> Shape<R> shape_of(const Grid& g) {
 }
 
 template <typename R>
-__global__ void k_ct_to_c128(size_t n, Lay L, int W, const typename CT<R>::C* __restrict__ a, double2* out) {
+__global__ void k_ct_to_c128(size_t n, Lay L, int W, const typename CT<R>::C* __restrict__ a, double2* out,
+                             int split_lgq = -1) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int y = (int)(i / W), x = (int)(i % W);
-    const auto v = a[L.at(y, x)];
+    const auto v = a[L.at(split_lgq >= 0 ? split_row(y, split_lgq) : y, x)];
     out[i] = make_double2((double)v.x, (double)v.y);
   }
 }
@@ -622,13 +699,24 @@ template <typename R> struct A2Op : OpBase {
   };
   // V_set is written row-major (once per item), so the A3 row pass reads
   // whole contiguous row blocks
+  // Split plans (vs_lgt >= 0): virtual column -> (column, plane), V stored
+  // row-major with plane c's rows at c * 2048 (the A3 row pass combines them)
+  int vs_lgt = -1, vs_W = 0;
   template <int LGN> struct FOut {
     const C* b;
     C* out;
     int W;
     int x0, lgS;
+    int vsl, Wp;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)]; }
-    template <int ST> LS_D void store(int seq, int j, int r, C v, int) { out[rm_col<LGN, ST>(W, j, r, x0 + seq)] = v; }
+    template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
+      if (vsl >= 0) {
+        const int xv = x0 + seq;
+        out[(size_t)((vs_plane(xv, vsl) << kLgVsM) + j + r * ST) * Wp + vs_col(xv, vsl)] = v;
+      } else {
+        out[rm_col<LGN, ST>(W, j, r, x0 + seq)] = v;
+      }
+    }
   };
   LS_D void end(State& S, int it, C* b, C*) const {
     const int set = set_of(it, lgnt), t = it & ((1 << lgnt) - 1);
@@ -639,7 +727,7 @@ template <typename R> struct A2Op : OpBase {
       constexpr int LGN = decltype(fx)::LGN;
       eng::for_last_slots<LGN, true, C>(g, PutAcc<LGN>{b, S, sh.lgS});
       __syncthreads();
-      FOut<LGN> f{b, dst, sh.W, t << sh.lgS, sh.lgS};
+      FOut<LGN> f{b, dst, sh.W, t << sh.lgS, sh.lgS, vs_lgt, vs_W};
       eng::run_fix<LGN, true, true>(g, b, tw, f);
     });
     __syncthreads();
@@ -663,7 +751,14 @@ template <typename R> struct A3Op : OpBase {
   double* dots;
   int ix0, ix1;  // dots over columns [ix0, ix1) ...
   int iy0, iy1;  // ... and rows [iy0, iy1)
+  int vs_lgq = -1;  // split plan: V rows in plane order, combined before the transform
   LS_D void prefetch(int it, int, C* b, C*) const {
+    if (vs_lgq >= 0) {  // plane rows c * 2048 + n2_0 + q: four strips of Q rows
+      for (int c = 0; c < 4; ++c)
+        eng::gather_rect<sizeof(C)>(b + ((c << vs_lgq) << sh.lgW), V0, sh.rm(),
+                                    vs_plane_row(c << vs_lgq, vs_lgq, it << vs_lgq), vs_lgq, 0, sh.lgW);
+      return;
+    }
     eng::gather_rect<sizeof(C)>(b, V0, sh.rm(), it << sh.lgR, sh.lgR, 0, sh.lgW);
   }
   template <int LGN> struct F {
@@ -675,17 +770,20 @@ template <typename R> struct A3Op : OpBase {
     const double* vp;
     State& S;
     int y0, lgn, W, ix0, ix1, iy0, iy1;
+    int lgq;  // split plan: buffer row -> natural row (v1 already folded in)
+    LS_D int row(int seq) const { return lgq >= 0 ? vs_row(seq, lgq, y0) : y0 + seq; }
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const C x = b[nat_row<LGN, ST>(seq, j, r, lgn)];
       if constexpr (LGN > 0) return v1 ? x + __ldg(&v1[rm_row<LGN, ST>(W, y0 + seq, j, r)]) : x;
       else return v1 ? x + __ldg(&v1[(size_t)(y0 + seq) * W + j]) : x;
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
-      const size_t p = rm_row<LGN, ST>(W, y0 + seq, j, r);
+      const int y = row(seq);
+      const size_t p = rm_row<LGN, ST>(W, y, j, r);
       const double val = scale * (double)v.x;
       out[p] = val;
       const int x = j + r * ST;
-      if (vp && x >= ix0 && x < ix1 && y0 + seq >= iy0 && y0 + seq < iy1) {
+      if (vp && x >= ix0 && x < ix1 && y >= iy0 && y < iy1) {
         const double q = vp[p];
         S.acc[0] += val * (val - q);
         S.acc[1] += q * q;
@@ -694,9 +792,15 @@ template <typename R> struct A3Op : OpBase {
   };
   LS_D void step(State& S, int it, int, C* b, C*) const {
     const Geo g = sh.grow();
+    if (vs_lgq >= 0) {
+      vs_inv_combine(b, sh.lgW, vs_lgq, it << vs_lgq, tw, sh.twsH, V1);
+      __syncthreads();
+    }
+    const C* v1 = vs_lgq >= 0 ? nullptr : V1;
+    const int y0 = vs_lgq >= 0 ? it << vs_lgq : it << sh.lgR;
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      F<LGN> f{b, V1, sh.rm(), scale, out, vp, S, it << sh.lgR, sh.lgW, sh.W, ix0, ix1, iy0, iy1};
+      F<LGN> f{b, v1, sh.rm(), scale, out, vp, S, y0, sh.lgW, sh.W, ix0, ix1, iy0, iy1, vs_lgq};
       eng::run_fix<LGN, false, true>(g, b, tw, f);
     });
   }
@@ -1059,17 +1163,28 @@ template <typename R> struct TMaskRowsOp : OpBase {
   int kind;
   const C* tw;
   alignas(64) CUtensorMap tmap_out;  // M~ (one column-tiled field), row boxes
+  int vs_lgq = -1;                   // split plan: log2 Q (rows per plane in an item)
   LS_D unsigned load_bytes() const { return (unsigned)((sh.W << sh.lgR) * (kind == SRC_U8 ? 1 : 8)); }
   LS_D void load(int it, int, C* dst, uint64_t* bar) const {
-    const size_t off = ((size_t)it << sh.lgR) * sh.W * (kind == SRC_U8 ? 1 : 8);
-    tma::bulk_g2s(dst, static_cast<const unsigned char*>(src) + off, load_bytes(), bar);
+    const int es = kind == SRC_U8 ? 1 : 8;
+    const unsigned char* s = static_cast<const unsigned char*>(src);
+    if (vs_lgq >= 0) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
+      const unsigned qb = (unsigned)(sh.W << vs_lgq) * es;
+      for (int m = 0; m < 4; ++m)
+        tma::bulk_g2s(reinterpret_cast<unsigned char*>(dst) + m * qb,
+                      s + (size_t)vs_row(m << vs_lgq, vs_lgq, it << vs_lgq) * sh.W * es, qb, bar);
+      return;
+    }
+    tma::bulk_g2s(dst, s + ((size_t)it << sh.lgR) * sh.W * es, load_bytes(), bar);
   }
   LS_D void store(int it, int, const C* src_s) const {
     constexpr int LGT = lg_tile<C>();
     const int y0 = it << sh.lgR, tiles = sh.W >> LGT, bt = tiles < 256 ? tiles : 256;
-    for (int r = 0; r < (1 << sh.lgR); ++r)
+    for (int r = 0; r < (1 << sh.lgR); ++r) {
+      const int y = vs_lgq >= 0 ? vs_plane_row(r, vs_lgq, it << vs_lgq) : y0 + r;
       for (int b = 0; b * bt < tiles; ++b)
-        tma::tensor_s2g(&tmap_out, 0, b * bt, y0 + r, 0, src_s + (r << sh.lgW) + ((b * bt) << LGT));
+        tma::tensor_s2g(&tmap_out, 0, b * bt, y, 0, src_s + (r << sh.lgW) + ((b * bt) << LGT));
+    }
   }
   template <int LGN> struct F {
     C* b;
@@ -1087,7 +1202,7 @@ template <typename R> struct TMaskRowsOp : OpBase {
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, false>(seq, j, r)] = v; }
   };
-  LS_D void step(State&, int, int, C* b, C*, unsigned) const {
+  LS_D void step(State&, int it, int, C* b, C*, unsigned) const {
     const Geo g = sh.grow();
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -1096,6 +1211,10 @@ template <typename R> struct TMaskRowsOp : OpBase {
         eng::run_fix<LGN, false, false>(g, b, tw, f);
       }
     });
+    if (vs_lgq >= 0) {
+      __syncthreads();
+      vs_fwd_combine(b, sh.lgW, vs_lgq, it << vs_lgq, tw, sh.twsH);
+    }
   }
 };
 
@@ -1149,6 +1268,7 @@ template <typename R> struct TF1Op : OpBase {
   alignas(64) CUtensorMap tmap_spec1;  // spectra of set 1
   alignas(64) CUtensorMap tmap_T;     // T fields, column-item boxes
   int koff[2];                      // first kernel index of each set in the stacked maps
+  int vs_lgt = -1;                  // split plan: the item's virtual columns map to (column, plane) (tmap_T physical)
   LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnt)]; }
   LS_D int kbase(int it) const { return grp_of(it, lgnt) * kpg; }
   LS_D unsigned load_bytes() const { return (unsigned)((sh.H << sh.lgS) * sizeof(C)); }
@@ -1165,9 +1285,10 @@ template <typename R> struct TF1Op : OpBase {
     });
   }
   LS_D void store(int it, int k, const C* src) const {
-    const int set = set_of(it, lgnt), x0 = (it & ((1 << lgnt) - 1)) << sh.lgS;
+    const int set = set_of(it, lgnt), xv = (it & ((1 << lgnt) - 1)) << sh.lgS;
+    const int x0 = vs_lgt >= 0 ? vs_col(xv, vs_lgt) : xv, y0 = vs_lgt >= 0 ? vs_plane(xv, vs_lgt) << kLgVsM : 0;
     col_boxes(x0, k + koff[set], kLgTileT, [&](int c0, int c1, int c2, int kk, int off) {
-      tma::tensor_s2g(&tmap_T, c0, c1, c2, kk, src + off);
+      tma::tensor_s2g(&tmap_T, c0, c1, y0 + c2, kk, src + off);
     });
   }
   // boxes of a column item: {min(S,w) words-per-elem, S/w tiles, 256 rows}
@@ -1217,24 +1338,34 @@ template <typename R> struct TF2Op : OpBase {
   const C* tw;
   int lgnb;
   int split_lgq;                   // >= 0: T rows stored in split order (split_row)
+  int vs_lgq = -1;                 // split plan (Grid::vsplit): log2 Q
   alignas(64) CUtensorMap tmap_T;  // T fields, row-item boxes
   int koff[2];
   LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnb)]; }
   LS_D int kbase(int it) const { return grp_of(it, lgnb) * kpg; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
   LS_D unsigned load_bytes() const { return (unsigned)((sh.W << sh.lgR) * sizeof(C)); }
+  LS_D int n20(int it) const { return (it & ((1 << lgnb) - 1)) << vs_lgq; }
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
     const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     const int tiles = sh.W >> kLgTileT, bt = tiles < 256 ? tiles : 256;
     for (int r = 0; r < (1 << sh.lgR); ++r) {
-      const int yr = split_lgq >= 0 ? split_row(y0 + r, split_lgq) : y0 + r;
+      const int yr = vs_lgq >= 0 ? vs_plane_row(r, vs_lgq, n20(it))
+                                 : split_lgq >= 0 ? split_row(y0 + r, split_lgq) : y0 + r;
       for (int b = 0; b * bt < tiles; ++b)
         tma::tensor_g2s(dst + (r << sh.lgW) + ((b * bt) << kLgTileT), &tmap_T, 0, b * bt, yr, k + koff[set], bar);
     }
   }
   LS_D void store(int it, int k, const C* src) const {
     const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
-    tma::bulk_s2g(a.A[set] + (size_t)k * fsz() + ((size_t)y0 << sh.lgW), src, load_bytes());
+    C* A = a.A[set] + (size_t)k * fsz();
+    if (vs_lgq >= 0) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
+      const unsigned qb = (unsigned)((sh.W << vs_lgq) * sizeof(C));
+      for (int m = 0; m < 4; ++m)
+        tma::bulk_s2g(A + ((size_t)vs_row(m << vs_lgq, vs_lgq, n20(it)) << sh.lgW), src + ((m << vs_lgq) << sh.lgW), qb);
+      return;
+    }
+    tma::bulk_s2g(A + ((size_t)y0 << sh.lgW), src, load_bytes());
   }
   LS_D void begin(State& S, int, C*) const {
 #pragma unroll
@@ -1252,6 +1383,10 @@ template <typename R> struct TF2Op : OpBase {
   };
   LS_D void step(State& S, int it, int k, C* b, C*, unsigned) const {
     const Geo g = sh.grow();
+    if (vs_lgq >= 0) {
+      vs_inv_combine(b, sh.lgW, vs_lgq, n20(it), tw, sh.twsH);
+      __syncthreads();
+    }
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       if constexpr (LGN > 0) {
@@ -1260,6 +1395,14 @@ template <typename R> struct TF2Op : OpBase {
       }
     });
   }
+  template <int LGN> struct WriteIS {  // split plan: buffer row -> natural row
+    R* I;
+    const State& S;
+    int lgq, n20, W;
+    template <int ST> LS_D void operator()(int seq, int j, int r, int slot) const {
+      I[rm_row<LGN, ST>(W, vs_row(seq, lgq, n20), j, r)] = S.acc[slot];
+    }
+  };
   LS_D void end(State& S, int it, C*, C*) const {
     const int set = set_of(it, lgnb), blk = it & ((1 << lgnb) - 1), y0 = blk << sh.lgR;
     const Geo g = sh.grow();
@@ -1267,7 +1410,10 @@ template <typename R> struct TF2Op : OpBase {
     R* dst = lgg ? a.Ipart + (size_t)((set << lgg) + grp_of(it, lgnb)) * n : a.I[set];
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      eng::for_last_slots<LGN, false, C>(g, typename F2Op<R>::template WriteI<LGN>{dst, S, y0, sh.W});
+      if (vs_lgq >= 0)
+        eng::for_last_slots<LGN, false, C>(g, WriteIS<LGN>{dst, S, vs_lgq, n20(it), sh.W});
+      else
+        eng::for_last_slots<LGN, false, C>(g, typename F2Op<R>::template WriteI<LGN>{dst, S, y0, sh.W});
     });
     if (lgg)
       group_combine(a.Ipart + (size_t)(set << lgg) * n, n, a.I[set], (size_t)y0 * sh.W, 1 << sh.lgR, sh.W, sh.W,
@@ -1288,28 +1434,52 @@ template <typename R> struct TA1Op : OpBase {
   int lgnb;
   alignas(64) CUtensorMap tmap_U;  // U fields (layout tile lg_tile<C>), row-item boxes
   int koff[2];
+  int vs_lgq = -1;                 // split plan (Grid::vsplit): log2 Q
   LS_D int steps(int it) const { return lgg ? kpg : a.nk[set_of(it, lgnb)]; }
   LS_D int kbase(int it) const { return grp_of(it, lgnb) * kpg; }
   LS_D size_t fsz() const { return (size_t)sh.H * sh.W; }
   LS_D unsigned load_bytes() const { return (unsigned)((sh.W << sh.lgR) * sizeof(C)); }
+  LS_D int n20(int it) const { return (it & ((1 << lgnb) - 1)) << vs_lgq; }
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
     const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
-    tma::bulk_g2s(dst, a.A[set] + (size_t)k * fsz() + ((size_t)y0 << sh.lgW), load_bytes(), bar);
+    const C* A = a.A[set] + (size_t)k * fsz();
+    if (vs_lgq >= 0) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
+      const unsigned qb = (unsigned)((sh.W << vs_lgq) * sizeof(C));
+      for (int m = 0; m < 4; ++m)
+        tma::bulk_g2s(dst + ((m << vs_lgq) << sh.lgW), A + ((size_t)vs_row(m << vs_lgq, vs_lgq, n20(it)) << sh.lgW),
+                      qb, bar);
+      return;
+    }
+    tma::bulk_g2s(dst, A + ((size_t)y0 << sh.lgW), load_bytes(), bar);
   }
   LS_D void store(int it, int k, const C* src) const {
     const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     constexpr int LGT = lg_tile<C>();
     const int tiles = sh.W >> LGT, bt = tiles < 256 ? tiles : 256;
-    for (int r = 0; r < (1 << sh.lgR); ++r)
+    for (int r = 0; r < (1 << sh.lgR); ++r) {
+      const int y = vs_lgq >= 0 ? vs_plane_row(r, vs_lgq, n20(it)) : y0 + r;
       for (int b = 0; b * bt < tiles; ++b)
-        tma::tensor_s2g(&tmap_U, 0, b * bt, y0 + r, k + koff[set], src + (r << sh.lgW) + ((b * bt) << LGT));
+        tma::tensor_s2g(&tmap_U, 0, b * bt, y, k + koff[set], src + (r << sh.lgW) + ((b * bt) << LGT));
+    }
   }
+  template <int LGN> struct LoadGS {  // split plan: buffer row -> natural row
+    State& S;
+    const R* gate;
+    int lgq, n20, W;
+    template <int ST> LS_D void operator()(int seq, int j, int r, int slot) const {
+      S.g[slot] = __ldg(&gate[rm_row<LGN, ST>(W, vs_row(seq, lgq, n20), j, r)]);
+    }
+  };
   LS_D void begin(State& S, int it, C*) const {
     const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     eng::dispatch<C>(sh.grow(), true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      if constexpr (LGN > 0)
-        eng::for_first_slots<LGN, false, C>(typename A1Op<R>::template LoadG<LGN>{S, a.gate[set], y0, sh.W});
+      if constexpr (LGN > 0) {
+        if (vs_lgq >= 0)
+          eng::for_first_slots<LGN, false, C>(LoadGS<LGN>{S, a.gate[set], vs_lgq, n20(it), sh.W});
+        else
+          eng::for_first_slots<LGN, false, C>(typename A1Op<R>::template LoadG<LGN>{S, a.gate[set], y0, sh.W});
+      }
     });
   }
   template <int LGN> struct F {
@@ -1320,7 +1490,7 @@ template <typename R> struct TA1Op : OpBase {
     }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) { b[nat_out<LGN, ST, C, false>(seq, j, r)] = v; }
   };
-  LS_D void step(State& S, int, int, C* b, C*, unsigned) const {
+  LS_D void step(State& S, int it, int, C* b, C*, unsigned) const {
     const Geo g = sh.grow();
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
@@ -1329,6 +1499,10 @@ template <typename R> struct TA1Op : OpBase {
         eng::run_fix<LGN, false, false>(g, b, tw, f);
       }
     });
+    if (vs_lgq >= 0) {
+      __syncthreads();
+      vs_fwd_combine(b, sh.lgW, vs_lgq, n20(it), tw, sh.twsH);
+    }
   }
 };
 
@@ -1823,8 +1997,10 @@ void mask_fft_impl(const Grid& g, const void* src, int kind, void* mhat, void* s
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   const size_t src_bytes = ((size_t)1 << sh.lgR) * g.W * (kind == SRC_U8 ? 1 : 8);
-  if (tma_ok_rows(sh) && src_bytes % 16 == 0 && src_bytes <= (size_t)row_bufE(sh) * sizeof(C) &&
-      reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+  const bool rows_tma = tma_ok_rows(sh) && src_bytes % 16 == 0 && src_bytes <= (size_t)row_bufE(sh) * sizeof(C) &&
+                        reinterpret_cast<uintptr_t>(src) % 16 == 0;
+  if (g.vsplit && !rows_tma) throw std::runtime_error("split plan: mask rows need the TMA path");
+  if (rows_tma) {
     TMaskRowsOp<R> mr;
     mr.sh = sh;
     mr.src = src;
@@ -1833,6 +2009,7 @@ void mask_fft_impl(const Grid& g, const void* src, int kind, void* mhat, void* s
     const int ew = sizeof(C) / 8, tiles = g.W >> sh.lgT;
     mr.tmap_out = make_field_map(TmaField{scratch, sh.lgT, ew}, g.H, g.W, 1, (unsigned)((1 << sh.lgT) * ew),
                                  (unsigned)std::min(tiles, 256), 1);
+    mr.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
     mr.bufE = tma_bufE<R>(row_bufE(sh));
     mr.nitems = g.H >> sh.lgR;
     launch_tma<R>(mr, row_threads(sh), stop, s);
@@ -1847,6 +2024,11 @@ void mask_fft_impl(const Grid& g, const void* src, int kind, void* mhat, void* s
     mr.nitems = g.H >> sh.lgR;
     launch_op<R>(mr, row_threads(sh), 0, stop, s);
   }
+  if (g.vsplit) {  // columns of the virtual 2048 x 4W grid
+    const Grid gv = vs_grid(g);
+    sh = shape_of<R>(gv);
+    if (!(tma_ok_cols(sh) && sh.lgS == sh.lgT)) throw std::runtime_error("split plan: columns need the TMA path");
+  }
   if (tma_ok_cols(sh) && sh.lgS == sh.lgT) {
     TColsOp<R> mc;
     mc.sh = sh;
@@ -1854,7 +2036,7 @@ void mask_fft_impl(const Grid& g, const void* src, int kind, void* mhat, void* s
     mc.out = static_cast<C*>(mhat);
     mc.tw = static_cast<const C*>(g.tw);
     mc.bufE = tma_bufE<R>(col_bufE(sh));
-    mc.nitems = g.W >> sh.lgS;
+    mc.nitems = sh.W >> sh.lgS;
     launch_tma<R>(mc, col_threads(sh), stop, s);
     return;
   }
@@ -1872,10 +2054,12 @@ void mask_fft_impl(const Grid& g, const void* src, int kind, void* mhat, void* s
 }
 
 template <typename R>
-void f1_impl(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s) {
+void f1_impl(const Grid& gp, const void* mhat, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s) {
   using C = typename CT<R>::C;
+  const Grid g = gp.vsplit ? vs_grid(gp) : gp;  // split plans: the virtual 2048 x 4W grid
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
+  if (gp.vsplit && !tma_ok_cols(sh)) throw std::runtime_error("split plan: F1 needs the TMA path");
   if (tma_ok_cols(sh)) {
     TF1Op<R> f1;
     f1.sh = sh;
@@ -1895,10 +2079,12 @@ void f1_impl(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, St
       if (i == 0) f1.tmap_spec = m; else f1.tmap_spec1 = m;
     }
     auto cbT = colbox(kLgTileT);
-    f1.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), cbT.first, cbT.second, rows);
+    // T_k keeps the physical layout (the F2 row pass reads plane rows by coordinates)
+    f1.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, gp.H, gp.W, total_nk(a), cbT.first, cbT.second, rows);
+    f1.vs_lgt = gp.vsplit ? sh.lgT : -1;
     for (int i = 0; i < 2; ++i) f1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     f1.bufE = tma_bufE<R>(col_bufE(sh));
-    f1.lgg = choose_lgg<R>((1 << f1.lgnt) * nsets, a);
+    f1.lgg = gp.vsplit ? 0 : choose_lgg<R>((1 << f1.lgnt) * nsets, a);
     f1.kpg = a.nk[0] >> f1.lgg;
     f1.nitems = ((1 << f1.lgnt) * nsets) << f1.lgg;
     launch_tma<R>(f1, col_threads(sh), stop, s);
@@ -1951,19 +2137,21 @@ void f2_impl(const Grid& g, const SpecSet* sets, int nsets, double2* a0_out, Sto
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
+  if (g.vsplit && !tma_ok_rows(sh)) throw std::runtime_error("split plan: F2 needs the TMA path");
   if (tma_ok_rows(sh)) {
     TF2Op<R> f2;
     f2.sh = sh;
     f2.a = a;
     f2.tw = static_cast<const C*>(g.tw);
     f2.lgnb = g.lgH - sh.lgR;
-    f2.split_lgq = split_ok(sh) ? 11 : -1;
+    f2.split_lgq = !g.vsplit && split_ok(sh) ? 11 : -1;
+    f2.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
     const int ew = sizeof(C) / 8, tiles = g.W >> kLgTileT;
     f2.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), (unsigned)((1 << kLgTileT) * ew),
                                (unsigned)std::min(tiles, 256), 1);
     for (int i = 0; i < 2; ++i) f2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     f2.bufE = tma_bufE<R>(row_bufE(sh));
-    f2.lgg = choose_lgg<R>((1 << f2.lgnb) * nsets, a);
+    f2.lgg = g.vsplit ? 0 : choose_lgg<R>((1 << f2.lgnb) * nsets, a);
     f2.kpg = a.nk[0] >> f2.lgg;
     f2.nitems = ((1 << f2.lgnb) * nsets) << f2.lgg;
     launch_tma<R>(f2, row_threads(sh), stop, s);
@@ -1986,8 +2174,10 @@ void a1_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
+  if (g.vsplit && !tma_ok_rows(sh)) throw std::runtime_error("split plan: A1 needs the TMA path");
   if (tma_ok_rows(sh)) {
     TA1Op<R> a1;
+    a1.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
     a1.sh = sh;
     a1.a = a;
     a1.tw = static_cast<const C*>(g.tw);
@@ -1997,7 +2187,7 @@ void a1_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
                                (unsigned)std::min(tiles, 256), 1);
     for (int i = 0; i < 2; ++i) a1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     a1.bufE = tma_bufE<R>(row_bufE(sh));
-    a1.lgg = choose_lgg<R>((1 << a1.lgnb) * nsets, a);
+    a1.lgg = g.vsplit ? 0 : choose_lgg<R>((1 << a1.lgnb) * nsets, a);
     a1.kpg = a.nk[0] >> a1.lgg;
     a1.nitems = ((1 << a1.lgnb) * nsets) << a1.lgg;
     launch_tma<R>(a1, row_threads(sh), stop, s);
@@ -2014,13 +2204,17 @@ void a1_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
 }
 
 template <typename R>
-void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s) {
+void a2_impl(const Grid& gp, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s) {
   using C = typename CT<R>::C;
+  const Grid g = gp.vsplit ? vs_grid(gp) : gp;  // split plans: the virtual 2048 x 4W grid
   Shape<R> sh = shape_of<R>(g);
   SetArgs<R> a = set_args<R>(g, sets, nsets);
+  if (gp.vsplit && !tma_ok_cols(sh)) throw std::runtime_error("split plan: A2 needs the TMA path");
   if (tma_ok_cols(sh)) {
     TA2Op<R> a2;
     a2.sh = sh;
+    a2.vs_lgt = gp.vsplit ? sh.lgT : -1;
+    a2.vs_W = gp.W;
     a2.a = a;
     a2.tw = static_cast<const C*>(g.tw);
     a2.lgnt = g.lgW - sh.lgS;
@@ -2036,7 +2230,7 @@ void a2_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
     }
     for (int i = 0; i < 2; ++i) a2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
     a2.bufE = tma_bufE<R>(col_bufE(sh));
-    a2.lgg = choose_lgg<R>((1 << a2.lgnt) * nsets, a);
+    a2.lgg = gp.vsplit ? 0 : choose_lgg<R>((1 << a2.lgnt) * nsets, a);
     a2.kpg = a.nk[0] >> a2.lgg;
     a2.nitems = ((1 << a2.lgnt) * nsets) << a2.lgg;
     launch_tma<R>(a2, col_threads(sh), stop, s);
@@ -2077,6 +2271,7 @@ int finish_impl(const Grid& g, const void* V0, const void* V1, double scale, dou
   a3.iy0 = iy0;
   a3.iy1 = iy1 < g.H ? iy1 : g.H;
   a3.tail = tail && vp ? *tail : LoopTail{};
+  a3.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
   a3.bufE = row_bufE(sh);
   a3.nitems = g.H >> sh.lgR;
   int grid = launch_op<R>(a3, row_threads(sh), 0, stop, s, finish_max_blocks());

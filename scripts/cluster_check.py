@@ -1,4 +1,4 @@
-"""Tall-grid column passes: cluster path vs single-column path (dev check).
+"""Tall-grid column passes: split plan / cluster paths vs the single-column path (dev check).
 Prints max relative difference of the loss history and the final-mask XOR."""
 import json, os, subprocess, sys
 from pathlib import Path
@@ -19,9 +19,11 @@ if len(sys.argv) > 1 and sys.argv[1] == "run":
 import numpy as np
 H, W = (int(a) for a in sys.argv[1:3]) if len(sys.argv) > 2 else (8192, 256)
 out = {}
-extra = sys.argv[3] if len(sys.argv) > 3 else ""          # e.g. LSOPC_B200_NO_SPLIT=1
-env_extra = dict([extra.split("=")]) if extra else {}
-for tag, env in (("cluster", env_extra), ("single", {"LSOPC_B200_NO_CLUSTER": "1"})):
+extra = sys.argv[3] if len(sys.argv) > 3 else ""          # e.g. LSOPC_B200_NO_VSPLIT=1,LSOPC_B200_NO_SPLIT=1
+env_extra = dict(kv.split("=") for kv in extra.split(",") if kv)
+# reference leg: the single-column cp.async column passes of the unsplit plan
+single = {"LSOPC_B200_NO_CLUSTER": "1", "LSOPC_B200_NO_VSPLIT": "1"}
+for tag, env in (("cluster", env_extra), ("single", single)):
     p = subprocess.run([sys.executable, __file__, "run", str(H), str(W), f"/tmp/cc_{tag}.npy"], capture_output=True,
                        text=True, env={**os.environ, **env})
     if p.returncode:

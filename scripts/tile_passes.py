@@ -1,7 +1,8 @@
 """Per-pass CUDA-event times (lsopc_session_time_passes) of one DSO iteration
-on tall / wide / square grids, fp32 tier, 24 + 24 kernels (configs[4]
-geometry study).  python scripts/tile_passes.py H W [H W ...]"""
+on tall / wide / square grids, 24 + 24 kernels (configs[4] geometry
+study).  [PREC=fp64] python scripts/tile_passes.py H W [H W ...]"""
 import ctypes
+import os
 import sys
 from pathlib import Path
 
@@ -14,7 +15,7 @@ import paper_2303_12529_b200 as b2  # noqa: E402
 from paper_2303_12529_b200 import _native as nv, inputs  # noqa: E402
 
 NAMES = ["mask", "F1", "F2", "resist", "A1", "A2", "A3", "ls"]
-nv.set_precision("fp32")
+nv.set_precision(os.environ.get("PREC", "fp32"))
 focus, defocus = b2.gen_synthetic_kernels(35, 24, seed=4)
 args = [int(a) for a in sys.argv[1:]] or [8192, 2048, 2048, 8192]
 for H, W in zip(args[::2], args[1::2]):

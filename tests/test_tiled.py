@@ -166,15 +166,16 @@ def test_strips_match_single_tile(world, axis):
 
 @pytest.mark.gpu
 def test_tall_grid_cluster_column_passes_match_single_column_path():
-    """8192-point columns (configs[4] windows) run F1 / A2 on 4-CTA clusters
-    (distributed-shared-memory column scatter, k_pass_cluster); the same
-    solve with the clusters disabled takes the single-column passes.  Inputs
-    bit-identical, outputs within float32 rounding."""
+    """8192-point columns (configs[4] windows): the split plan (default; 2048-
+    point virtual-grid column passes), and with it disabled the 4-CTA cluster
+    passes (k_pass_cluster, with and without the four-step F1 k_f1_split),
+    each against the single-column cp.async passes.  Inputs bit-identical,
+    outputs within float32 rounding."""
     import subprocess
     import sys
     from pathlib import Path
     script = Path(__file__).resolve().parents[1] / "scripts" / "cluster_check.py"
-    for extra in ([], ["LSOPC_B200_NO_SPLIT=1"]):  # four-step split F1, then the single-column cluster F1
+    for extra in ([], ["LSOPC_B200_NO_VSPLIT=1"], ["LSOPC_B200_NO_VSPLIT=1,LSOPC_B200_NO_SPLIT=1"]):
         p = subprocess.run([sys.executable, str(script), "8192", "256", *extra], capture_output=True, text=True,
                            timeout=600)
         assert p.returncode == 0, p.stdout + p.stderr
