@@ -209,7 +209,12 @@ int lsopc_dsn_init(size_t n, const float* phi_raw_dev, const float* m_raw_dev, d
  * max |v_total|, max |grad phi| (max), [6] max step (max)), which the caller
  * combines across ranks before the next phase; after phase 4 the caller
  * refreshes the halo columns of lsopc_session_phi_ptr().  Forward phases
- * threshold phi directly, so only phi needs exchanging. */
+ * threshold phi directly, so only phi needs exchanging.
+ * Phase 1 = phase 6 (stop rule, best iterate) then phase 5 (adjoint, dot
+ * partials).  Several strips sharing one plan's work fields in one process
+ * run 0, 5 per strip back to back (the adjoint reads only the forward's
+ * fields, never the stop decision's outputs), combine losses and dots
+ * together, then 6, 2, 3, 4 per strip. */
 int lsopc_session_set_tile(lsopc_session* s, int ix0, int ix1, int xlo, int xhi);
 /* The general strip window: interior [iy0, iy1) x [ix0, ix1), stencil
  * neighbours bounded by [ylo, yhi) x [xlo, xhi).  Full-width strips (rows

@@ -37,7 +37,10 @@ namespace eng {
 // complex128 (<= 255 registers), i.e. 64 KB of operands per stage buffer.
 template <typename C> constexpr int P_of() { return 16; }
 template <typename C> constexpr int LGP_of() { return 4; }
-template <typename C> constexpr int cta_threads() { return sizeof(C) == 8 ? 512 : 256; }
+#ifndef LSB_C64_THREADS  // experiment builds may shrink the complex64 CTA (LSB_DEFINES=-DLSB_C64_THREADS=256)
+#define LSB_C64_THREADS 512
+#endif
+template <typename C> constexpr int cta_threads() { return sizeof(C) == 8 ? LSB_C64_THREADS : 256; }
 
 // ---- radix-R DFTs in registers, forward sign (exp(-2 pi i rk/R)), natural order out
 
@@ -388,7 +391,7 @@ LS_D void run_stages(C (&v)[P_of<C>()], C* sm, const C* tw, int tws, F& f) {
   if constexpr (SI + 1 < PL::nst) run_stages<LGN, LGS, SI + 1, COLS, INV>(v, sm, tw, tws, f);
 }
 
-template <typename C> constexpr int lg_full() { return sizeof(C) == 8 ? 13 : 12; }  // log2(cta_threads * P)
+template <typename C> constexpr int lg_full() { return sizeof(C) == 8 && LSB_C64_THREADS == 512 ? 13 : 12; }  // log2(cta_threads * P)
 constexpr int kFastMinLgn = 8;
 
 // (seq, idx) of slot `slot` in the last stage (fast path)

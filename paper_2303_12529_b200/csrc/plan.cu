@@ -631,10 +631,15 @@ void enqueue_phase(lsopc_session* ss, int phase, cudaStream_t s) {
                     nullptr, t.iy0, t.iy1);
       launch_reduce_partials(p->partials.as<double>(), reduce_blocks(), 4, 0, sc, s);
     } break;
-    case 1: {  // stop rule on the global losses; adjoint -> sum PR dots
+    case 1:    // stop rule on the global losses; adjoint -> sum PR dots
+    case 6: {  // 6: the stop rule alone (after phase 5)
       LoopCfg lc{c.alpha, c.beta, c.stop_rel_tol, c.stop_patience};
       launch_after_forward(sc, 1, lc, st, ss->hist.as<double>(), s);
       launch_copy_best(n, ss->phi.as<double>(), ss->best.as<double>(), st, s);
+      if (phase == 6) break;
+    }
+      [[fallthrough]];
+    case 5: {  // 5: the adjoint alone, straight after phase 0 (it reads only the forward's fields)
       launch_a1(g, sets, 2, stop, s);
       launch_a2(g, sets, 2, stop, s);
       const int nd = launch_adjoint_finish(g, p->V0.p, p->V1.p, 4.0 * c.sigma_z / (double)n, v, vprev,
@@ -932,7 +937,7 @@ int lsopc_session_set_window(lsopc_session* ss, int ix0, int ix1, int xlo, int x
 int lsopc_session_phase(lsopc_session* ss, int phase) {
   return guarded([&] {
     if (!ss || !ss->tiled) throw Error(LSOPC_EINVAL, "phases need a strip session (lsopc_session_set_tile)");
-    if (phase < 0 || phase > 4) throw Error(LSOPC_EINVAL, "phase must be 0..4");
+    if (phase < 0 || phase > 6) throw Error(LSOPC_EINVAL, "phase must be 0..6");
     if (phase == 0 && ss->it >= ss->cfg.max_iters) throw Error(LSOPC_EINVAL, "max_iters reached");
     enqueue_phase(ss, phase, ss->s);
     if (phase == 4) ++ss->it;

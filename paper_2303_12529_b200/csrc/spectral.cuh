@@ -640,7 +640,7 @@ template <typename R> struct A1Op : OpBase {
 };
 
 // A2: V_set = IFFT_y( sum_k w_k conj(H_k) . FFT_y U_k )
-template <typename R> struct A2Op : OpBase {
+template <typename R, bool VS = false> struct A2Op : OpBase {
   using C = typename CT<R>::C;
   static constexpr int P = eng::P_of<C>();
   struct State { C acc[P]; };
@@ -699,7 +699,7 @@ template <typename R> struct A2Op : OpBase {
   };
   // V_set is written row-major (once per item), so the A3 row pass reads
   // whole contiguous row blocks
-  // Split plans (vs_lgt >= 0): virtual column -> (column, plane), V stored
+  // Split plans (VS): virtual column -> (column, plane), V stored
   // row-major with plane c's rows at c * 2048 (the A3 row pass combines them)
   int vs_lgt = -1, vs_W = 0;
   template <int LGN> struct FOut {
@@ -710,7 +710,7 @@ template <typename R> struct A2Op : OpBase {
     int vsl, Wp;
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const { return b[nat_col<LGN, ST, C>(seq, j, r, lgS)]; }
     template <int ST> LS_D void store(int seq, int j, int r, C v, int) {
-      if (vsl >= 0) {
+      if constexpr (VS) {
         const int xv = x0 + seq;
         out[(size_t)((vs_plane(xv, vsl) << kLgVsM) + j + r * ST) * Wp + vs_col(xv, vsl)] = v;
       } else {
@@ -738,7 +738,7 @@ template <typename R> struct A2Op : OpBase {
 };
 
 // A3: out = scale * Re IFFT_x(V_0 [+ V_1]) (f64 row-major) + CG dot partials per CTA
-template <typename R> struct A3Op : OpBase {
+template <typename R, bool VS = false> struct A3Op : OpBase {
   using C = typename CT<R>::C;
   struct State { double acc[2]; };
   Shape<R> sh;
@@ -753,7 +753,7 @@ template <typename R> struct A3Op : OpBase {
   int iy0, iy1;  // ... and rows [iy0, iy1)
   int vs_lgq = -1;  // split plan: V rows in plane order, combined before the transform
   LS_D void prefetch(int it, int, C* b, C*) const {
-    if (vs_lgq >= 0) {  // plane rows c * 2048 + n2_0 + q: four strips of Q rows
+    if constexpr (VS) {  // plane rows c * 2048 + n2_0 + q: four strips of Q rows
       for (int c = 0; c < 4; ++c)
         eng::gather_rect<sizeof(C)>(b + ((c << vs_lgq) << sh.lgW), V0, sh.rm(),
                                     vs_plane_row(c << vs_lgq, vs_lgq, it << vs_lgq), vs_lgq, 0, sh.lgW);
@@ -771,7 +771,7 @@ template <typename R> struct A3Op : OpBase {
     State& S;
     int y0, lgn, W, ix0, ix1, iy0, iy1;
     int lgq;  // split plan: buffer row -> natural row (v1 already folded in)
-    LS_D int row(int seq) const { return lgq >= 0 ? vs_row(seq, lgq, y0) : y0 + seq; }
+    LS_D int row(int seq) const { return VS ? vs_row(seq, lgq, y0) : y0 + seq; }
     template <int ST> LS_D C load(int seq, int j, int r, int slot) const {
       const C x = b[nat_row<LGN, ST>(seq, j, r, lgn)];
       if constexpr (LGN > 0) return v1 ? x + __ldg(&v1[rm_row<LGN, ST>(W, y0 + seq, j, r)]) : x;
@@ -792,12 +792,12 @@ template <typename R> struct A3Op : OpBase {
   };
   LS_D void step(State& S, int it, int, C* b, C*) const {
     const Geo g = sh.grow();
-    if (vs_lgq >= 0) {
+    if constexpr (VS) {
       vs_inv_combine(b, sh.lgW, vs_lgq, it << vs_lgq, tw, sh.twsH, V1);
       __syncthreads();
     }
-    const C* v1 = vs_lgq >= 0 ? nullptr : V1;
-    const int y0 = vs_lgq >= 0 ? it << vs_lgq : it << sh.lgR;
+    const C* v1 = VS ? nullptr : V1;
+    const int y0 = VS ? it << vs_lgq : it << sh.lgR;
     eng::dispatch<C>(g, sh.fast(), [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       F<LGN> f{b, v1, sh.rm(), scale, out, vp, S, y0, sh.lgW, sh.W, ix0, ix1, iy0, iy1, vs_lgq};
@@ -1153,7 +1153,7 @@ template <int LGN, int STRIDE, typename C, bool COLS> LS_D int nat_out(int seq, 
 // mask / phi) arrive by one 1-D bulk copy; the transform reads them from
 // shared memory in the first stage; M~ rows leave by per-row tensor boxes
 // into the column-tiled scratch (like TA1's U_k stores).
-template <typename R> struct TMaskRowsOp : OpBase {
+template <typename R, bool VS = false> struct TMaskRowsOp : OpBase {
   using C = typename CT<R>::C;
   using State = NoState;
   static constexpr bool kStores = true;
@@ -1168,7 +1168,7 @@ template <typename R> struct TMaskRowsOp : OpBase {
   LS_D void load(int it, int, C* dst, uint64_t* bar) const {
     const int es = kind == SRC_U8 ? 1 : 8;
     const unsigned char* s = static_cast<const unsigned char*>(src);
-    if (vs_lgq >= 0) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
+    if constexpr (VS) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
       const unsigned qb = (unsigned)(sh.W << vs_lgq) * es;
       for (int m = 0; m < 4; ++m)
         tma::bulk_g2s(reinterpret_cast<unsigned char*>(dst) + m * qb,
@@ -1181,7 +1181,7 @@ template <typename R> struct TMaskRowsOp : OpBase {
     constexpr int LGT = lg_tile<C>();
     const int y0 = it << sh.lgR, tiles = sh.W >> LGT, bt = tiles < 256 ? tiles : 256;
     for (int r = 0; r < (1 << sh.lgR); ++r) {
-      const int y = vs_lgq >= 0 ? vs_plane_row(r, vs_lgq, it << vs_lgq) : y0 + r;
+      const int y = VS ? vs_plane_row(r, vs_lgq, it << vs_lgq) : y0 + r;
       for (int b = 0; b * bt < tiles; ++b)
         tma::tensor_s2g(&tmap_out, 0, b * bt, y, 0, src_s + (r << sh.lgW) + ((b * bt) << LGT));
     }
@@ -1211,7 +1211,7 @@ template <typename R> struct TMaskRowsOp : OpBase {
         eng::run_fix<LGN, false, false>(g, b, tw, f);
       }
     });
-    if (vs_lgq >= 0) {
+    if constexpr (VS) {
       __syncthreads();
       vs_fwd_combine(b, sh.lgW, vs_lgq, it << vs_lgq, tw, sh.twsH);
     }
@@ -1251,7 +1251,7 @@ template <typename R> struct TColsOp : OpBase {
 };
 
 // TF1: T_k = IFFT_y(M^ . H_k)/(HW); H_k tile in by TMA, T_k slab out by TMA
-template <typename R> struct TF1Op : OpBase {
+template <typename R, bool VS = false> struct TF1Op : OpBase {
   using C = typename CT<R>::C;
   static constexpr int P = eng::P_of<C>();
   static constexpr bool kStores = true;
@@ -1286,7 +1286,7 @@ template <typename R> struct TF1Op : OpBase {
   }
   LS_D void store(int it, int k, const C* src) const {
     const int set = set_of(it, lgnt), xv = (it & ((1 << lgnt) - 1)) << sh.lgS;
-    const int x0 = vs_lgt >= 0 ? vs_col(xv, vs_lgt) : xv, y0 = vs_lgt >= 0 ? vs_plane(xv, vs_lgt) << kLgVsM : 0;
+    const int x0 = VS ? vs_col(xv, vs_lgt) : xv, y0 = VS ? vs_plane(xv, vs_lgt) << kLgVsM : 0;
     col_boxes(x0, k + koff[set], kLgTileT, [&](int c0, int c1, int c2, int kk, int off) {
       tma::tensor_s2g(&tmap_T, c0, c1, y0 + c2, kk, src + off);
     });
@@ -1327,7 +1327,7 @@ template <typename R> struct TF1Op : OpBase {
 };
 
 // TF2: A_k = IFFT_x T_k (out by 1-D bulk), I_set = sum w |A_k|^2 (registers)
-template <typename R> struct TF2Op : OpBase {
+template <typename R, bool VS = false> struct TF2Op : OpBase {
   using C = typename CT<R>::C;
   static constexpr int P = eng::P_of<C>();
   static constexpr bool kStores = true;
@@ -1350,7 +1350,7 @@ template <typename R> struct TF2Op : OpBase {
     const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     const int tiles = sh.W >> kLgTileT, bt = tiles < 256 ? tiles : 256;
     for (int r = 0; r < (1 << sh.lgR); ++r) {
-      const int yr = vs_lgq >= 0 ? vs_plane_row(r, vs_lgq, n20(it))
+      const int yr = VS ? vs_plane_row(r, vs_lgq, n20(it))
                                  : split_lgq >= 0 ? split_row(y0 + r, split_lgq) : y0 + r;
       for (int b = 0; b * bt < tiles; ++b)
         tma::tensor_g2s(dst + (r << sh.lgW) + ((b * bt) << kLgTileT), &tmap_T, 0, b * bt, yr, k + koff[set], bar);
@@ -1359,7 +1359,7 @@ template <typename R> struct TF2Op : OpBase {
   LS_D void store(int it, int k, const C* src) const {
     const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     C* A = a.A[set] + (size_t)k * fsz();
-    if (vs_lgq >= 0) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
+    if constexpr (VS) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
       const unsigned qb = (unsigned)((sh.W << vs_lgq) * sizeof(C));
       for (int m = 0; m < 4; ++m)
         tma::bulk_s2g(A + ((size_t)vs_row(m << vs_lgq, vs_lgq, n20(it)) << sh.lgW), src + ((m << vs_lgq) << sh.lgW), qb);
@@ -1383,7 +1383,7 @@ template <typename R> struct TF2Op : OpBase {
   };
   LS_D void step(State& S, int it, int k, C* b, C*, unsigned) const {
     const Geo g = sh.grow();
-    if (vs_lgq >= 0) {
+    if constexpr (VS) {
       vs_inv_combine(b, sh.lgW, vs_lgq, n20(it), tw, sh.twsH);
       __syncthreads();
     }
@@ -1410,7 +1410,7 @@ template <typename R> struct TF2Op : OpBase {
     R* dst = lgg ? a.Ipart + (size_t)((set << lgg) + grp_of(it, lgnb)) * n : a.I[set];
     eng::dispatch<C>(g, true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
-      if (vs_lgq >= 0)
+      if constexpr (VS)
         eng::for_last_slots<LGN, false, C>(g, WriteIS<LGN>{dst, S, vs_lgq, n20(it), sh.W});
       else
         eng::for_last_slots<LGN, false, C>(g, typename F2Op<R>::template WriteI<LGN>{dst, S, y0, sh.W});
@@ -1422,7 +1422,7 @@ template <typename R> struct TF2Op : OpBase {
 };
 
 // TA1: U_k = FFT_x(gate . A_k): A_k rows in by 1-D bulk, U_k rows out by tensor map
-template <typename R> struct TA1Op : OpBase {
+template <typename R, bool VS = false> struct TA1Op : OpBase {
   using C = typename CT<R>::C;
   static constexpr int P = eng::P_of<C>();
   static constexpr bool kStores = true;
@@ -1443,7 +1443,7 @@ template <typename R> struct TA1Op : OpBase {
   LS_D void load(int it, int k, C* dst, uint64_t* bar) const {
     const int set = set_of(it, lgnb), y0 = (it & ((1 << lgnb) - 1)) << sh.lgR;
     const C* A = a.A[set] + (size_t)k * fsz();
-    if (vs_lgq >= 0) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
+    if constexpr (VS) {  // natural rows n2_0 + q + 2048 m: four strips of Q rows
       const unsigned qb = (unsigned)((sh.W << vs_lgq) * sizeof(C));
       for (int m = 0; m < 4; ++m)
         tma::bulk_g2s(dst + ((m << vs_lgq) << sh.lgW), A + ((size_t)vs_row(m << vs_lgq, vs_lgq, n20(it)) << sh.lgW),
@@ -1457,7 +1457,7 @@ template <typename R> struct TA1Op : OpBase {
     constexpr int LGT = lg_tile<C>();
     const int tiles = sh.W >> LGT, bt = tiles < 256 ? tiles : 256;
     for (int r = 0; r < (1 << sh.lgR); ++r) {
-      const int y = vs_lgq >= 0 ? vs_plane_row(r, vs_lgq, n20(it)) : y0 + r;
+      const int y = VS ? vs_plane_row(r, vs_lgq, n20(it)) : y0 + r;
       for (int b = 0; b * bt < tiles; ++b)
         tma::tensor_s2g(&tmap_U, 0, b * bt, y, k + koff[set], src + (r << sh.lgW) + ((b * bt) << LGT));
     }
@@ -1475,7 +1475,7 @@ template <typename R> struct TA1Op : OpBase {
     eng::dispatch<C>(sh.grow(), true, [&](auto fx) {
       constexpr int LGN = decltype(fx)::LGN;
       if constexpr (LGN > 0) {
-        if (vs_lgq >= 0)
+        if constexpr (VS)
           eng::for_first_slots<LGN, false, C>(LoadGS<LGN>{S, a.gate[set], vs_lgq, n20(it), sh.W});
         else
           eng::for_first_slots<LGN, false, C>(typename A1Op<R>::template LoadG<LGN>{S, a.gate[set], y0, sh.W});
@@ -1499,7 +1499,7 @@ template <typename R> struct TA1Op : OpBase {
         eng::run_fix<LGN, false, false>(g, b, tw, f);
       }
     });
-    if (vs_lgq >= 0) {
+    if constexpr (VS) {
       __syncthreads();
       vs_fwd_combine(b, sh.lgW, vs_lgq, n20(it), tw, sh.twsH);
     }
@@ -1511,9 +1511,9 @@ template <typename R> struct TA1Op : OpBase {
 // and holds H_k of the current step (TMA, own mbarrier), which the last
 // butterfly stage reads from shared memory.  H_k of step q+1 is requested as
 // soon as step q's last stage has read its operand slot, a full step ahead.
-template <typename R> struct TA2Op : A2Op<R> {
+template <typename R, bool VS = false> struct TA2Op : A2Op<R, VS> {
   using C = typename CT<R>::C;
-  using State = typename A2Op<R>::State;
+  using State = typename A2Op<R, VS>::State;
   static constexpr int P = eng::P_of<C>();
   static constexpr bool kStores = false;
   static constexpr bool kSideLoad = true;
@@ -1989,6 +1989,13 @@ template <typename R> int choose_lgg(int base_items, const SetArgs<R>& a) {
   return lgg;
 }
 
+// split plans instantiate the ops with VS = true (compile-time: the unsplit
+// passes keep their exact code)
+template <class Fn> void with_vs(bool vs, Fn&& fn) {
+  if (vs) fn(std::true_type{});
+  else fn(std::false_type{});
+}
+
 // ---------------------------------------------------------------------------
 
 template <typename R>
@@ -2001,18 +2008,20 @@ void mask_fft_impl(const Grid& g, const void* src, int kind, void* mhat, void* s
                         reinterpret_cast<uintptr_t>(src) % 16 == 0;
   if (g.vsplit && !rows_tma) throw std::runtime_error("split plan: mask rows need the TMA path");
   if (rows_tma) {
-    TMaskRowsOp<R> mr;
-    mr.sh = sh;
-    mr.src = src;
-    mr.kind = kind;
-    mr.tw = static_cast<const C*>(g.tw);
-    const int ew = sizeof(C) / 8, tiles = g.W >> sh.lgT;
-    mr.tmap_out = make_field_map(TmaField{scratch, sh.lgT, ew}, g.H, g.W, 1, (unsigned)((1 << sh.lgT) * ew),
-                                 (unsigned)std::min(tiles, 256), 1);
-    mr.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
-    mr.bufE = tma_bufE<R>(row_bufE(sh));
-    mr.nitems = g.H >> sh.lgR;
-    launch_tma<R>(mr, row_threads(sh), stop, s);
+    with_vs(g.vsplit, [&](auto vs) {
+      TMaskRowsOp<R, decltype(vs)::value> mr;
+      mr.sh = sh;
+      mr.src = src;
+      mr.kind = kind;
+      mr.tw = static_cast<const C*>(g.tw);
+      const int ew = sizeof(C) / 8, tiles = g.W >> sh.lgT;
+      mr.tmap_out = make_field_map(TmaField{scratch, sh.lgT, ew}, g.H, g.W, 1, (unsigned)((1 << sh.lgT) * ew),
+                                   (unsigned)std::min(tiles, 256), 1);
+      mr.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
+      mr.bufE = tma_bufE<R>(row_bufE(sh));
+      mr.nitems = g.H >> sh.lgR;
+      launch_tma<R>(mr, row_threads(sh), stop, s);
+    });
   } else {
     MaskRowsOp<R> mr;
     mr.sh = sh;
@@ -2061,33 +2070,35 @@ void f1_impl(const Grid& gp, const void* mhat, const SpecSet* sets, int nsets, S
   SetArgs<R> a = set_args<R>(g, sets, nsets);
   if (gp.vsplit && !tma_ok_cols(sh)) throw std::runtime_error("split plan: F1 needs the TMA path");
   if (tma_ok_cols(sh)) {
-    TF1Op<R> f1;
-    f1.sh = sh;
-    f1.a = a;
-    f1.mhat = static_cast<const C*>(mhat);
-    f1.scale = (R)(1.0 / (double)g.n());
-    f1.tw = static_cast<const C*>(g.tw);
-    f1.lgnt = g.lgW - sh.lgS;
-    f1.spec_lgw = sh.lgT;
-    const int ew = sizeof(C) / 8, S = 1 << sh.lgS, rows = std::min(g.H, 256);
-    auto colbox = [&](int lgw) { return std::make_pair((unsigned)(std::min(S, 1 << lgw) * ew),
-                                                         (unsigned)std::max(1, S >> lgw)); };
-    // spectra of each set: separate allocations -> separate maps (koff 0)
-    for (int i = 0; i < nsets; ++i) {
-      auto cb = colbox(sh.lgT);
-      CUtensorMap m = make_field_map(TmaField{a.spec[i], sh.lgT, ew}, g.H, g.W, a.nk[i], cb.first, cb.second, rows);
-      if (i == 0) f1.tmap_spec = m; else f1.tmap_spec1 = m;
-    }
-    auto cbT = colbox(kLgTileT);
-    // T_k keeps the physical layout (the F2 row pass reads plane rows by coordinates)
-    f1.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, gp.H, gp.W, total_nk(a), cbT.first, cbT.second, rows);
-    f1.vs_lgt = gp.vsplit ? sh.lgT : -1;
-    for (int i = 0; i < 2; ++i) f1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
-    f1.bufE = tma_bufE<R>(col_bufE(sh));
-    f1.lgg = gp.vsplit ? 0 : choose_lgg<R>((1 << f1.lgnt) * nsets, a);
-    f1.kpg = a.nk[0] >> f1.lgg;
-    f1.nitems = ((1 << f1.lgnt) * nsets) << f1.lgg;
-    launch_tma<R>(f1, col_threads(sh), stop, s);
+    with_vs(gp.vsplit, [&](auto vs) {
+      TF1Op<R, decltype(vs)::value> f1;
+      f1.sh = sh;
+      f1.a = a;
+      f1.mhat = static_cast<const C*>(mhat);
+      f1.scale = (R)(1.0 / (double)g.n());
+      f1.tw = static_cast<const C*>(g.tw);
+      f1.lgnt = g.lgW - sh.lgS;
+      f1.spec_lgw = sh.lgT;
+      const int ew = sizeof(C) / 8, S = 1 << sh.lgS, rows = std::min(g.H, 256);
+      auto colbox = [&](int lgw) { return std::make_pair((unsigned)(std::min(S, 1 << lgw) * ew),
+                                                           (unsigned)std::max(1, S >> lgw)); };
+      // spectra of each set: separate allocations -> separate maps (koff 0)
+      for (int i = 0; i < nsets; ++i) {
+        auto cb = colbox(sh.lgT);
+        CUtensorMap m = make_field_map(TmaField{a.spec[i], sh.lgT, ew}, g.H, g.W, a.nk[i], cb.first, cb.second, rows);
+        if (i == 0) f1.tmap_spec = m; else f1.tmap_spec1 = m;
+      }
+      auto cbT = colbox(kLgTileT);
+      // T_k keeps the physical layout (the F2 row pass reads plane rows by coordinates)
+      f1.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, gp.H, gp.W, total_nk(a), cbT.first, cbT.second, rows);
+      f1.vs_lgt = gp.vsplit ? sh.lgT : -1;
+      for (int i = 0; i < 2; ++i) f1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+      f1.bufE = tma_bufE<R>(col_bufE(sh));
+      f1.lgg = gp.vsplit ? 0 : choose_lgg<R>((1 << f1.lgnt) * nsets, a);
+      f1.kpg = a.nk[0] >> f1.lgg;
+      f1.nitems = ((1 << f1.lgnt) * nsets) << f1.lgg;
+      launch_tma<R>(f1, col_threads(sh), stop, s);
+    });
     return;
   }
   F1Op<R> f1;
@@ -2139,22 +2150,24 @@ void f2_impl(const Grid& g, const SpecSet* sets, int nsets, double2* a0_out, Sto
   SetArgs<R> a = set_args<R>(g, sets, nsets);
   if (g.vsplit && !tma_ok_rows(sh)) throw std::runtime_error("split plan: F2 needs the TMA path");
   if (tma_ok_rows(sh)) {
-    TF2Op<R> f2;
-    f2.sh = sh;
-    f2.a = a;
-    f2.tw = static_cast<const C*>(g.tw);
-    f2.lgnb = g.lgH - sh.lgR;
-    f2.split_lgq = !g.vsplit && split_ok(sh) ? 11 : -1;
-    f2.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
-    const int ew = sizeof(C) / 8, tiles = g.W >> kLgTileT;
-    f2.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), (unsigned)((1 << kLgTileT) * ew),
-                               (unsigned)std::min(tiles, 256), 1);
-    for (int i = 0; i < 2; ++i) f2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
-    f2.bufE = tma_bufE<R>(row_bufE(sh));
-    f2.lgg = g.vsplit ? 0 : choose_lgg<R>((1 << f2.lgnb) * nsets, a);
-    f2.kpg = a.nk[0] >> f2.lgg;
-    f2.nitems = ((1 << f2.lgnb) * nsets) << f2.lgg;
-    launch_tma<R>(f2, row_threads(sh), stop, s);
+    with_vs(g.vsplit, [&](auto vs) {
+      TF2Op<R, decltype(vs)::value> f2;
+      f2.sh = sh;
+      f2.a = a;
+      f2.tw = static_cast<const C*>(g.tw);
+      f2.lgnb = g.lgH - sh.lgR;
+      f2.split_lgq = !g.vsplit && split_ok(sh) ? 11 : -1;
+      f2.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
+      const int ew = sizeof(C) / 8, tiles = g.W >> kLgTileT;
+      f2.tmap_T = make_field_map(TmaField{a.T[0], kLgTileT, ew}, g.H, g.W, total_nk(a), (unsigned)((1 << kLgTileT) * ew),
+                                 (unsigned)std::min(tiles, 256), 1);
+      for (int i = 0; i < 2; ++i) f2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+      f2.bufE = tma_bufE<R>(row_bufE(sh));
+      f2.lgg = g.vsplit ? 0 : choose_lgg<R>((1 << f2.lgnb) * nsets, a);
+      f2.kpg = a.nk[0] >> f2.lgg;
+      f2.nitems = ((1 << f2.lgnb) * nsets) << f2.lgg;
+      launch_tma<R>(f2, row_threads(sh), stop, s);
+    });
   } else {
     F2Op<R> f2;
     f2.sh = sh;
@@ -2176,21 +2189,23 @@ void a1_impl(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaS
   SetArgs<R> a = set_args<R>(g, sets, nsets);
   if (g.vsplit && !tma_ok_rows(sh)) throw std::runtime_error("split plan: A1 needs the TMA path");
   if (tma_ok_rows(sh)) {
-    TA1Op<R> a1;
-    a1.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
-    a1.sh = sh;
-    a1.a = a;
-    a1.tw = static_cast<const C*>(g.tw);
-    a1.lgnb = g.lgH - sh.lgR;
-    const int ew = sizeof(C) / 8, tiles = g.W >> sh.lgT;
-    a1.tmap_U = make_field_map(TmaField{a.T[0], sh.lgT, ew}, g.H, g.W, total_nk(a), (unsigned)((1 << sh.lgT) * ew),
-                               (unsigned)std::min(tiles, 256), 1);
-    for (int i = 0; i < 2; ++i) a1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
-    a1.bufE = tma_bufE<R>(row_bufE(sh));
-    a1.lgg = g.vsplit ? 0 : choose_lgg<R>((1 << a1.lgnb) * nsets, a);
-    a1.kpg = a.nk[0] >> a1.lgg;
-    a1.nitems = ((1 << a1.lgnb) * nsets) << a1.lgg;
-    launch_tma<R>(a1, row_threads(sh), stop, s);
+    with_vs(g.vsplit, [&](auto vs) {
+      TA1Op<R, decltype(vs)::value> a1;
+      a1.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
+      a1.sh = sh;
+      a1.a = a;
+      a1.tw = static_cast<const C*>(g.tw);
+      a1.lgnb = g.lgH - sh.lgR;
+      const int ew = sizeof(C) / 8, tiles = g.W >> sh.lgT;
+      a1.tmap_U = make_field_map(TmaField{a.T[0], sh.lgT, ew}, g.H, g.W, total_nk(a), (unsigned)((1 << sh.lgT) * ew),
+                                 (unsigned)std::min(tiles, 256), 1);
+      for (int i = 0; i < 2; ++i) a1.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+      a1.bufE = tma_bufE<R>(row_bufE(sh));
+      a1.lgg = g.vsplit ? 0 : choose_lgg<R>((1 << a1.lgnb) * nsets, a);
+      a1.kpg = a.nk[0] >> a1.lgg;
+      a1.nitems = ((1 << a1.lgnb) * nsets) << a1.lgg;
+      launch_tma<R>(a1, row_threads(sh), stop, s);
+    });
     return;
   }
   A1Op<R> a1;
@@ -2211,29 +2226,31 @@ void a2_impl(const Grid& gp, const SpecSet* sets, int nsets, StopFlag stop, cuda
   SetArgs<R> a = set_args<R>(g, sets, nsets);
   if (gp.vsplit && !tma_ok_cols(sh)) throw std::runtime_error("split plan: A2 needs the TMA path");
   if (tma_ok_cols(sh)) {
-    TA2Op<R> a2;
-    a2.sh = sh;
-    a2.vs_lgt = gp.vsplit ? sh.lgT : -1;
-    a2.vs_W = gp.W;
-    a2.a = a;
-    a2.tw = static_cast<const C*>(g.tw);
-    a2.lgnt = g.lgW - sh.lgS;
-    a2.u_lgw = sh.lgT;
-    const int ew = sizeof(C) / 8, S = 1 << sh.lgS, w = 1 << sh.lgT;
-    a2.tmap_U = make_field_map(TmaField{a.T[0], sh.lgT, ew}, g.H, g.W, total_nk(a), (unsigned)(std::min(S, w) * ew),
-                               (unsigned)std::max(1, S / w), (unsigned)std::min(g.H, 256));
-    for (int i = 0; i < nsets; ++i) {
-      CUtensorMap m = make_field_map(TmaField{a.spec[i], sh.lgT, ew}, g.H, g.W, a.nk[i],
-                                     (unsigned)(std::min(S, w) * ew), (unsigned)std::max(1, S / w),
-                                     (unsigned)std::min(g.H, 256));
-      if (i == 0) a2.tmap_spec = m; else a2.tmap_spec1 = m;
-    }
-    for (int i = 0; i < 2; ++i) a2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
-    a2.bufE = tma_bufE<R>(col_bufE(sh));
-    a2.lgg = gp.vsplit ? 0 : choose_lgg<R>((1 << a2.lgnt) * nsets, a);
-    a2.kpg = a.nk[0] >> a2.lgg;
-    a2.nitems = ((1 << a2.lgnt) * nsets) << a2.lgg;
-    launch_tma<R>(a2, col_threads(sh), stop, s);
+    with_vs(gp.vsplit, [&](auto vs) {
+      TA2Op<R, decltype(vs)::value> a2;
+      a2.sh = sh;
+      a2.vs_lgt = gp.vsplit ? sh.lgT : -1;
+      a2.vs_W = gp.W;
+      a2.a = a;
+      a2.tw = static_cast<const C*>(g.tw);
+      a2.lgnt = g.lgW - sh.lgS;
+      a2.u_lgw = sh.lgT;
+      const int ew = sizeof(C) / 8, S = 1 << sh.lgS, w = 1 << sh.lgT;
+      a2.tmap_U = make_field_map(TmaField{a.T[0], sh.lgT, ew}, g.H, g.W, total_nk(a), (unsigned)(std::min(S, w) * ew),
+                                 (unsigned)std::max(1, S / w), (unsigned)std::min(g.H, 256));
+      for (int i = 0; i < nsets; ++i) {
+        CUtensorMap m = make_field_map(TmaField{a.spec[i], sh.lgT, ew}, g.H, g.W, a.nk[i],
+                                       (unsigned)(std::min(S, w) * ew), (unsigned)std::max(1, S / w),
+                                       (unsigned)std::min(g.H, 256));
+        if (i == 0) a2.tmap_spec = m; else a2.tmap_spec1 = m;
+      }
+      for (int i = 0; i < 2; ++i) a2.koff[i] = i < nsets ? set_koff(a, i, g.n()) : 0;
+      a2.bufE = tma_bufE<R>(col_bufE(sh));
+      a2.lgg = gp.vsplit ? 0 : choose_lgg<R>((1 << a2.lgnt) * nsets, a);
+      a2.kpg = a.nk[0] >> a2.lgg;
+      a2.nitems = ((1 << a2.lgnt) * nsets) << a2.lgg;
+      launch_tma<R>(a2, col_threads(sh), stop, s);
+    });
     return;
   }
   A2Op<R> a2;
@@ -2257,24 +2274,27 @@ int finish_impl(const Grid& g, const void* V0, const void* V1, double scale, dou
                 int iy1) {
   using C = typename CT<R>::C;
   Shape<R> sh = shape_of<R>(g);
-  A3Op<R> a3;
-  a3.sh = sh;
-  a3.V0 = static_cast<const C*>(V0);
-  a3.V1 = static_cast<const C*>(V1);
-  a3.tw = static_cast<const C*>(g.tw);
-  a3.scale = scale;
-  a3.out = out;
-  a3.vp = vp;
-  a3.dots = dots;
-  a3.ix0 = ix0;
-  a3.ix1 = ix1 > 0 ? ix1 : g.W;
-  a3.iy0 = iy0;
-  a3.iy1 = iy1 < g.H ? iy1 : g.H;
-  a3.tail = tail && vp ? *tail : LoopTail{};
-  a3.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
-  a3.bufE = row_bufE(sh);
-  a3.nitems = g.H >> sh.lgR;
-  int grid = launch_op<R>(a3, row_threads(sh), 0, stop, s, finish_max_blocks());
+  int grid = 0;
+  with_vs(g.vsplit, [&](auto vs) {
+    A3Op<R, decltype(vs)::value> a3;
+    a3.sh = sh;
+    a3.V0 = static_cast<const C*>(V0);
+    a3.V1 = static_cast<const C*>(V1);
+    a3.tw = static_cast<const C*>(g.tw);
+    a3.scale = scale;
+    a3.out = out;
+    a3.vp = vp;
+    a3.dots = dots;
+    a3.ix0 = ix0;
+    a3.ix1 = ix1 > 0 ? ix1 : g.W;
+    a3.iy0 = iy0;
+    a3.iy1 = iy1 < g.H ? iy1 : g.H;
+    a3.tail = tail && vp ? *tail : LoopTail{};
+    a3.vs_lgq = g.vsplit ? sh.lgR - 2 : -1;
+    a3.bufE = row_bufE(sh);
+    a3.nitems = g.H >> sh.lgR;
+    grid = launch_op<R>(a3, row_threads(sh), 0, stop, s, finish_max_blocks());
+  });
   return vp ? grid : 0;
 }
 

@@ -58,6 +58,76 @@ def test_strip_geometry():
     assert tiled.strip_geometry(1024, 64, 4, 0, 35, axis=0).stencil_bounds() == (128, 512)
 
 
+def test_strip_layout_and_auto_strips():
+    """Several strips per rank: unequal interiors (floor(i L / n)) with one
+    common window; the automatic count minimises the window area per rank
+    among windows of 512..2048 lines (fp32) or a legal fp64 plan (8192 x
+    <=1024, column strips)."""
+    for L, n, K in [(8192, 5, 35), (8192, 9, 35), (1024, 3, 35), (1000, 7, 17)]:
+        strips = tiled.strip_layout(64, L, n, K)
+        assert len({s.ww for s in strips}) == 1
+        covered = np.concatenate([np.arange(s.x0, s.x1) for s in strips])
+        assert np.array_equal(covered, np.arange(L))
+        for s in strips:
+            i0, i1 = s.interior
+            assert i0 >= s.halo and s.ww - i1 >= s.halo
+            assert np.array_equal(s.columns()[i0:i1], np.arange(s.x0, s.x1))
+    assert [s.ww for s in tiled.strip_layout(64, 8192, 5, 35)][0] == 2048
+    assert tiled.auto_strips(8192, 8192, 1, 35, 0, "fp32") == 9   # 9 x 1024-line windows
+    assert tiled.auto_strips(8192, 8192, 8, 35, 0, "fp32") == 3   # 3 x 512 per rank
+    assert tiled.auto_strips(8192, 8192, 2, 35, 0, "fp32") == 5
+    assert tiled.auto_strips(8192, 8192, 1, 35, 1, "fp64") == 9   # 8192 x 1024, split plan
+    assert tiled.auto_strips(256, 1024, 1, 35, 1, "fp64") == 1
+    assert tiled.auto_strips(256, 1024, 2, 35, 1, "fp32") == 1
+    with pytest.raises(ValueError):
+        tiled.auto_strips(8192, 8192, 1, 35, 0, "fp64")  # complex128 rows stop at 4096 points
+
+
+def test_local_halo_exchange():
+    """Strips held by one process refresh each other's halos (ring)."""
+    for axis in (1, 0):
+        strips = tiled.strip_layout(8, 1000, 5, 17, 1) if axis == 1 else tiled.strip_layout(1000, 8, 5, 17, 0)
+        phis = []
+        for s in strips:
+            p = torch.full((8, s.ww), -1.0, dtype=torch.float64)
+            i0, i1 = s.interior
+            p[:, i0:i1] = torch.as_tensor(s.columns()[i0:i1], dtype=torch.float64)
+            phis.append(p.t().contiguous() if axis == 0 else p)
+        tiled.exchange_local_halos(phis, strips, wrap=True)
+        for s, p in zip(strips, phis):
+            p = p.t() if axis == 0 else p
+            i0, i1 = s.interior
+            h = s.halo
+            assert np.array_equal(p[:, i0 - h:i1 + h].numpy(),
+                                  np.broadcast_to(s.columns()[i0 - h:i1 + h], (8, i1 - i0 + 2 * h)))
+
+
+def _multi_halo_worker(rank, world, port, q, W, K, m):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = tiled.strip_layout(8, W, world * m, K)[rank * m:(rank + 1) * m]
+        phis = []
+        for s in mine:
+            p = torch.full((8, s.ww), -1.0, dtype=torch.float64)
+            i0, i1 = s.interior
+            p[:, i0:i1] = torch.as_tensor(s.columns()[i0:i1], dtype=torch.float64)
+            phis.append(p)
+        tiled.exchange_local_halos(phis, mine, wrap=False)
+        tiled.exchange_halos(phis[0], mine[0], tags=False, last=(phis[-1], mine[-1]))
+        q.put((rank, [p.numpy() for p in phis], [(s.columns(), s.interior, s.halo) for s in mine]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo_exchange_several_strips_per_rank_gloo():
+    """Two ranks x three strips: device-local copies inside a rank, positional
+    P2P (no tags) between the ranks' edge strips, wrapping."""
+    for rank, phis, geo in _run(2, _multi_halo_worker, 1200, 17, 3):
+        for p, (cols, (i0, i1), h) in zip(phis, geo):
+            assert np.array_equal(p[:, i0 - h:i1 + h], np.broadcast_to(cols[i0 - h:i1 + h], (8, i1 - i0 + 2 * h)))
+
+
 def _halo_worker(rank, world, port, q, W, K, tags, axis=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -162,6 +232,30 @@ def test_strips_match_single_tile(world, axis):
         assert np.allclose(h, hr, rtol=1e-9, atol=1e-12)
         assert np.array_equal(mask, mr)
         assert (l2r, pvbr) == (l2, pvb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("axis", [0, 1])
+def test_several_strips_in_one_process_match_single_tile(axis):
+    """One process runs the tile as three strips (shared plan, phases 0/5 per
+    strip, then the stop rule): the same history up to summation order, the
+    same final mask and L2 / PVB as the single-tile optimize."""
+    import paper_2303_12529_b200 as b2
+    from paper_2303_12529_b200 import _native as nv
+    nv.set_precision("fp64")
+    t, f, d = _case()
+    if axis == 0:
+        t = np.ascontiguousarray(t.T)
+    F, D = _ks(f, "focus"), _ks(d, "defocus")
+    r = tiled.optimize_tiled(t, F, D, b2.OptConfig(max_iters=12), axis=axis, strips_per_rank=3)
+    assert r.strips == 3 and r.window == ((256, 512) if axis == 1 else (512, 256))
+    rr = b2.optimize(t, F, D, b2.OptConfig(max_iters=12))
+    h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
+    hr = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in rr.loss_history])
+    assert h.shape == hr.shape
+    assert np.allclose(h, hr, rtol=1e-9, atol=1e-12)
+    assert np.array_equal(r.final_mask, rr.final_mask)
+    assert (r.metrics.l2, r.metrics.pvband) == (rr.metrics.l2, rr.metrics.pvband)
 
 
 @pytest.mark.gpu
