@@ -273,7 +273,7 @@ def time_session(b2, nv, L, sp, focus, defocus, target, K, W, precision, world, 
 
 def time_e2e(b2, target, focus, defocus, K, precision, reps=3):
     """`b2.optimize` from a host uint8 target with K iterations (H2D, TSDF,
-    K iterations, final prints, D2H of best phi + mask, host shot count): one
+    K iterations, final prints, D2H of best phi + mask, device shot count): one
     warm-up call, then the median of `reps` (seconds)."""
     import torch
     cfg = b2.OptConfig(max_iters=K, stop_patience=10**9, precision=precision)
@@ -548,7 +548,7 @@ def b200_arm(args, world, rank, local):
         "e2e": {"value": round(e2e_val, 3), "unit": "iters/s",
                 "h2d_bytes_per_step": round(n / K), "d2h_bytes_per_step": round(9 * n / K),
                 "note": f"b2.optimize(host uint8 target, max_iters={K}): H2D target, TSDF, {K} iterations, "
-                        f"final prints, D2H best phi + mask, host shot count; median of 3 = {t_e2e:.3f} s"},
+                        f"final prints, D2H best phi + mask, device shot count (lsopc_fracture_dev); median of 3 = {t_e2e:.3f} s"},
         # the roofline unit is one whole DSO iteration (one graph replay of
         # its launches): SURVEY §8(d) B_iter = n (64 N_k + 170) B (fp32 tier)
         # over the measured mean step time; the per-pass table beside it
