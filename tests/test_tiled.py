@@ -128,6 +128,29 @@ def test_halo_exchange_several_strips_per_rank_gloo():
             assert np.array_equal(p[:, i0 - h:i1 + h], np.broadcast_to(cols[i0 - h:i1 + h], (8, i1 - i0 + 2 * h)))
 
 
+def _gather_worker(rank, world, port, q, axis):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 5 + 2 * rank  # interiors of different extent per rank
+        t = torch.arange(3 * n, dtype=torch.float64).reshape((3, n) if axis == 1 else (n, 3)) + 100 * rank
+        q.put((rank, [x.numpy() for x in tiled._all_gather_var(t, axis)]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_all_gather_of_unequal_interiors(axis):
+    """The NCCL assembly path pads each rank's interior block to the widest
+    and trims it back (strip interiors differ by a line when n does not
+    divide the tile)."""
+    for rank, parts in _run(2, _gather_worker, axis):
+        for r, x in enumerate(parts):
+            n = 5 + 2 * r
+            ref = np.arange(3 * n, dtype=np.float64).reshape((3, n) if axis == 1 else (n, 3)) + 100 * r
+            assert np.array_equal(x, ref)
+
+
 def _halo_worker(rank, world, port, q, W, K, tags, axis=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -253,6 +276,29 @@ def test_several_strips_in_one_process_match_single_tile(axis):
     h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
     hr = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in rr.loss_history])
     assert h.shape == hr.shape
+    assert np.allclose(h, hr, rtol=1e-9, atol=1e-12)
+    assert np.array_equal(r.final_mask, rr.final_mask)
+    assert (r.metrics.l2, r.metrics.pvband) == (rr.metrics.l2, rr.metrics.pvband)
+
+
+@pytest.mark.gpu
+def test_fp64_column_strips_through_split_plan_match_single_grid():
+    """The fp64 configs[4] path in miniature: an 8192 x 1024 tile as three
+    8192 x 512 column windows (split plan, complex128) against the same tile
+    solved as one 8192 x 1024 split-plan grid (itself pinned to the oracle
+    at 8192 x 256, test_tall_parity.py): history rtol 1e-9, same mask."""
+    import paper_2303_12529_b200 as b2
+    from paper_2303_12529_b200 import _native as nv, inputs
+    nv.set_precision("fp64")
+    t = np.ascontiguousarray(inputs.mosaic_tile(range(16), grid=(4, 4))[:, 2048:3072])
+    fa, da = inputs.synthetic_kernel_arrays(35, 24, 4)
+    F, D = _ks(fa, "focus"), _ks(da, "defocus")
+    cfg = b2.OptConfig(max_iters=6, stop_patience=10**9)
+    r = tiled.optimize_tiled(t, F, D, cfg, axis=1, strips_per_rank=3)
+    assert r.strips == 3 and r.window == (8192, 512)
+    rr = b2.optimize(t, F, D, cfg)
+    h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
+    hr = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in rr.loss_history])
     assert np.allclose(h, hr, rtol=1e-9, atol=1e-12)
     assert np.array_equal(r.final_mask, rr.final_mask)
     assert (r.metrics.l2, r.metrics.pvband) == (rr.metrics.l2, rr.metrics.pvband)
