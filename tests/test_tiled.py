@@ -305,6 +305,32 @@ def test_fp64_column_strips_through_split_plan_match_single_grid():
 
 
 @pytest.mark.gpu
+def test_configs4_tile_strips_match_full_grid_8192():
+    """configs[4] at full size (parity against the single-GPU
+    full-grid 8192^2 run): the 8192^2 mosaic as nine 1024 x 8192 strips in
+    one process against the same tile optimised as one 8192^2 grid, fp32
+    tier, 4 iterations.  The two runs use different transform lengths along
+    y, so they agree to float32 rounding: losses rtol 1e-4, maxima 1e-3,
+    and final masks within a handful of threshold pixels."""
+    import paper_2303_12529_b200 as b2
+    from paper_2303_12529_b200 import inputs
+    tile = inputs.mosaic_tile(range(16), grid=(4, 4))
+    focus, defocus = b2.gen_synthetic_kernels(35, 24, seed=4)
+    cfg = b2.OptConfig(max_iters=4, stop_patience=10**9, precision="fp32")
+    r = tiled.optimize_tiled(tile, focus, defocus, cfg)
+    assert r.strips == 9 and r.window == (1024, 8192)
+    rr = b2.optimize(tile, focus, defocus, cfg)
+    h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
+    hr = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in rr.loss_history])
+    assert h.shape == hr.shape == (4, 7)
+    assert np.allclose(h[:, :3], hr[:, :3], rtol=1e-4), (h[:, :3], hr[:, :3])
+    assert np.allclose(h[:, 3:], hr[:, 3:], rtol=1e-3), (h[:, 3:], hr[:, 3:])
+    flips = int((r.final_mask != rr.final_mask).sum())
+    assert flips <= 64, flips
+    assert abs(r.metrics.l2 - rr.metrics.l2) <= 64 and abs(r.metrics.pvband - rr.metrics.pvband) <= 64
+
+
+@pytest.mark.gpu
 def test_tall_grid_cluster_column_passes_match_single_column_path():
     """8192-point columns (configs[4] windows): the split plan (default; 2048-
     point virtual-grid column passes), and with it disabled the 4-CTA cluster
