@@ -341,11 +341,15 @@ def test_tall_grid_cluster_column_passes_match_single_column_path():
     import sys
     from pathlib import Path
     script = Path(__file__).resolve().parents[1] / "scripts" / "cluster_check.py"
-    for extra in ([], ["LSOPC_B200_NO_VSPLIT=1"], ["LSOPC_B200_NO_VSPLIT=1,LSOPC_B200_NO_SPLIT=1"]):
-        p = subprocess.run([sys.executable, str(script), "8192", "256", *extra], capture_output=True, text=True,
+    # 8192 x 2048: the split plan with one row per plane in an item (Q = 1); float32 rounding of the two
+    # paths' different transform orders shows at 7e-6 there (the cluster path differs by the same amount)
+    legs = [("256", [], 1e-6), ("256", ["LSOPC_B200_NO_VSPLIT=1"], 1e-6),
+            ("256", ["LSOPC_B200_NO_VSPLIT=1,LSOPC_B200_NO_SPLIT=1"], 1e-6), ("2048", [], 2e-5)]
+    for width, extra, tol in legs:
+        p = subprocess.run([sys.executable, str(script), "8192", width, *extra], capture_output=True, text=True,
                            timeout=600)
         assert p.returncode == 0, p.stdout + p.stderr
         line = p.stdout.strip().splitlines()[-1]
         rel = float(line.split("rel diff ")[1].split(",")[0])
-        assert rel <= 1e-6, (extra, line)
+        assert rel <= tol, (extra, line)
         assert line.endswith("final mask xor 0"), (extra, line)
