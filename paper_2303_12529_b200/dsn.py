@@ -131,7 +131,7 @@ def instant_opc(targets, focus_kernels, defocus_kernels, cfg, net=None):
     phi0, m = dsn_init(x.float() + 100.0 * phi_raw.float().squeeze(1), m_raw.float().squeeze(1), cfg)
     sync()
     t3 = time.perf_counter()
-    parts = [_optimize_device(t, focus_kernels, defocus_kernels, cfg, phi0=phi0[i], modulation=m[i])
+    parts = [_optimize_device(t, focus_kernels, defocus_kernels, cfg, phi0=phi0[i], modulation=m[i], shots_on="host")
              for i, t in enumerate(targets)]
     sync()
     t4 = time.perf_counter()

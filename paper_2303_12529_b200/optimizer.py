@@ -341,11 +341,14 @@ def _device_inputs(target, focus_kernels, defocus_kernels, cfg, phi0, modulation
     return target, fk, dk, _device_f64(phi0, shape, "phi0"), _device_f64(modulation, shape, "modulation")
 
 
-def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=None):
+def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, modulation=None, shots_on="device"):
     """Device part of `optimize`: the loop, final prints and the device-to-host
     copies.  Returns the pieces `_assemble` turns into an OptimizationResult
     (split so a batch driver can overlap one clip's host tail with the next
-    clip's device loop)."""
+    clip's device loop).  shots_on="host": batch drivers, whose next clip's
+    persistent passes hold every SM, count shots with the host implementation
+    on a tail thread instead of the device kernel (one thread-block cluster
+    that would otherwise wait for, and then delay, those passes)."""
     t0 = time.perf_counter()
     if _is_device_tensor(phi0) or _is_device_tensor(modulation):
         target, fk, dk, p0, mdv = _device_inputs(target, focus_kernels, defocus_kernels, cfg, phi0, modulation)
@@ -372,7 +375,8 @@ def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, mod
     # the ctypes call releases the GIL) while the mask and the float64 phi are
     # copied straight into page-locked host tensors from torch's caching host
     # allocator, whose numpy views are the returned arrays (no host-side copy).
-    shots = _tail_pool().submit(_device_shots, fmask, nv.side_stream())
+    if shots_on == "device":
+        shots = _tail_pool().submit(_device_shots, fmask, nv.side_stream())
     t = nv.torch()
     mask_h = t.empty(shape, dtype=t.uint8, pin_memory=True)
     phi_h = t.empty(shape, dtype=t.float64, pin_memory=True)
@@ -380,6 +384,8 @@ def _optimize_device(target, focus_kernels, defocus_kernels, cfg, phi0=None, mod
     phi_h.copy_(best, non_blocking=True)
     t.cuda.current_stream().synchronize()
     wall = time.perf_counter() - t0
+    if shots_on != "device":
+        shots = _tail_pool().submit(shot_count, mask_h.numpy())
     return mask_h.numpy(), phi_h.numpy(), (res.iters, res.l2, res.pvband), hist, wall, shots
 
 

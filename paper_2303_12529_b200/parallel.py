@@ -118,7 +118,7 @@ def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, sol
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
                 for i, target in items:
-                    r = _assemble(_optimize_device(target, focus_kernels, defocus_kernels, cfg), cfg)
+                    r = _assemble(_optimize_device(target, focus_kernels, defocus_kernels, cfg, shots_on="host"), cfg)
                     with lock:
                         record(i, r)
             stream.synchronize()
