@@ -425,7 +425,8 @@ def b200_arm(args, world, rank, local):
         from paper_2303_12529_b200 import dsn
         net = dsn.build_net()
         cfg_d = b2.OptConfig(precision=args.precision)
-        dsn.instant_opc([inputs.iccad_like_clip(seed=900)], focus, defocus, cfg_d, net=net)  # warm-up
+        dsn.instant_opc([inputs.iccad_like_clip(seed=900 + j) for j in range(2)], focus, defocus, cfg_d,
+                        net=net)  # warm-up (both lanes)
         batch_t = [inputs.iccad_like_clip(seed=500 + rank * args.dsn_batch + i) for i in range(args.dsn_batch)]
         ri = dsn.instant_opc(batch_t, focus, defocus, cfg_d, net=net)
         lat = parallel.max_over_ranks(ri.latency, device="cuda")

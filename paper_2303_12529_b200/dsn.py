@@ -108,10 +108,51 @@ class InstantOPCResult:
         return self.t_tsdf + self.t_net + self.t_init + self.t_dso
 
 
-def instant_opc(targets, focus_kernels, defocus_kernels, cfg, net=None):
-    """configs[3]: DSN prediction for a batch of targets followed by the GPU
-    level-set refinement of each target.  Stage times are device-synchronised."""
+def refine_batch(targets, phi0, m, focus_kernels, defocus_kernels, cfg, lanes=2):
+    """The device level-set refinement of each target from its device phi0 /
+    modulation, on `lanes` worker threads with their own CUDA streams and work
+    buffers (like parallel.optimize_batch): one clip's host-side gaps overlap
+    another's device loop.  Results do not depend on `lanes`."""
     from .optimizer import _assemble, _optimize_device
+    torch = _torch()
+    results = [None] * len(targets)
+
+    def solve(i):
+        return _assemble(_optimize_device(targets[i], focus_kernels, defocus_kernels, cfg, phi0=phi0[i],
+                                          modulation=m[i], shots_on="host"), cfg)
+
+    lanes = max(1, min(int(lanes), len(targets)))
+    if lanes == 1:
+        for i in range(len(targets)):
+            results[i] = solve(i)
+        return results
+    from concurrent.futures import ThreadPoolExecutor
+    from . import _native as nv
+    dev = torch.cuda.current_device()
+    producer = torch.cuda.current_stream()
+
+    def worker(lane):
+        nv.set_lane(lane)
+        torch.cuda.set_device(dev)
+        stream = torch.cuda.Stream()
+        stream.wait_stream(producer)  # phi0 / m were written on the caller's stream
+        with torch.cuda.stream(stream):
+            for i in range(lane, len(targets), lanes):
+                results[i] = solve(i)
+        stream.synchronize()
+
+    with ThreadPoolExecutor(max_workers=lanes) as pool:
+        for f in [pool.submit(worker, lane) for lane in range(lanes)]:
+            f.result()
+    return results
+
+
+def instant_opc(targets, focus_kernels, defocus_kernels, cfg, net=None, lanes=2):
+    """configs[3]: DSN prediction for a batch of targets followed by the GPU
+    level-set refinement of each target.  Stage times are device-synchronised.
+    The refinements run on `lanes` worker threads with their own CUDA streams
+    and work buffers (like parallel.optimize_batch), so one clip's host-side
+    gaps overlap another's device loop; results do not depend on `lanes`."""
     torch = _torch()
     net = net or build_net()
 
@@ -131,9 +172,7 @@ def instant_opc(targets, focus_kernels, defocus_kernels, cfg, net=None):
     phi0, m = dsn_init(x.float() + 100.0 * phi_raw.float().squeeze(1), m_raw.float().squeeze(1), cfg)
     sync()
     t3 = time.perf_counter()
-    parts = [_optimize_device(t, focus_kernels, defocus_kernels, cfg, phi0=phi0[i], modulation=m[i], shots_on="host")
-             for i, t in enumerate(targets)]
+    results = refine_batch(targets, phi0, m, focus_kernels, defocus_kernels, cfg, lanes)
     sync()
     t4 = time.perf_counter()
-    results = [_assemble(p, cfg) for p in parts]
     return InstantOPCResult(results, t1 - t0, t2 - t1, t3 - t2, t4 - t3)

@@ -45,6 +45,17 @@ def test_instant_opc_small_batch():
     net = dsn.build_net(base=8, depth=3)
     r = dsn.instant_opc(targets, F, D, b2.OptConfig(max_iters=8), net=net)
     assert len(r.results) == 3 and r.latency > 0
+    # the refinement on two lanes (the default) equals one lane bit for bit
+    import torch
+    cfg = b2.OptConfig(max_iters=8)
+    x = dsn.tsdf_batch(targets, cfg.d_upper, cfg.d_lower)
+    phi0 = x.float().contiguous()
+    m = torch.full_like(phi0, 0.5)
+    r2 = dsn.refine_batch(targets, phi0, m, F, D, cfg, lanes=2)
+    r1 = dsn.refine_batch(targets, phi0, m, F, D, cfg, lanes=1)
+    for a, b in zip(r2, r1):
+        assert np.array_equal(a.final_mask, b.final_mask) and np.array_equal(a.final_phi.phi, b.final_phi.phi)
+        assert [h.l_dso for h in a.loss_history] == [h.l_dso for h in b.loss_history]
     for res, t in zip(r.results, targets):
         assert res.final_mask.shape == t.shape and set(np.unique(res.final_mask)) <= {0, 1}
         assert 1 <= res.iters_run <= 8
