@@ -4,6 +4,7 @@
 direct K0 spectra build, the radix-4 plane combine inside the row passes and
 2048-point column passes on the virtual 2048 x 4W grid -- in both tiers.
 8192-point rows (256 x 8192) take the tall-row TMA row passes (fp32).
+4096-point sides (the fp64 tier's largest single-plan sides) are checked too.
 Everything is checked against the numpy oracle on the same inputs with the
 production kernel model (24 + 24 kernels, K = 35, seed 4):
 
@@ -30,7 +31,9 @@ pytestmark = pytest.mark.gpu
 b2 = pytest.importorskip("paper_2303_12529_b200")
 from paper_2303_12529_b200 import _native as nv  # noqa: E402
 
-CASES = [("fp32", (8192, 256)), ("fp32", (256, 8192)), ("fp64", (8192, 256))]
+CASES = [("fp32", (8192, 256)), ("fp32", (256, 8192)), ("fp64", (8192, 256)),
+         # 4096-point sides: complex128 single-column passes / one-row items, complex64 half-width items
+         ("fp64", (4096, 256)), ("fp64", (256, 4096)), ("fp32", (4096, 256))]
 TOL = {"fp32": dict(i=1e-5, p=1e-5, g=2e-5, h=1e-4, v=1e-3),
        "fp64": dict(i=1e-10, p=1e-10, g=1e-9, h=1e-8, v=1e-8)}
 
