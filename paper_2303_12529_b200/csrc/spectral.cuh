@@ -1027,7 +1027,9 @@ template <typename R> struct F1COp : F1Op<R> {
 };
 
 // ---------------------------------------------------------------------------
-// Column passes on tall grids (8192-point columns, configs[4]): a column
+// Column passes on tall grids wider than the split plan takes (8192-point
+// columns with W > 2048 fp32, e.g. a whole 8192^2 tile as one grid; or with
+// LSOPC_B200_NO_VSPLIT=1 -- split plans run 2048-point columns): a column
 // item is one complex64 column, an 8-byte-wide slab of the 4-wide tiles, too
 // narrow for TMA; per-element cp.async / stores make the pass LSU-bound.
 // Here the four CTAs of a cluster take the four columns of one tile: each
@@ -1661,7 +1663,8 @@ int launch_tma(Op& op, int threads, StopFlag stop, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// Tall grids, four-step split (H = 4M, M = 2048, complex64): the column
+// Tall grids outside the split plan (see the column-pass note above), F1 as a
+// four-step split across the cluster (H = 4M, M = 2048, complex64): the column
 // transform of a 4-column tile is split across the 4-CTA cluster so every
 // CTA runs the fast 4-column 2048-point engine.  With f = f2 + M c and
 // n = 4 m + k1 (N = 4M):
