@@ -67,6 +67,34 @@ def threads():
     nv.set_precision(old)
 
 
+# the oracle's results depend only on the shape (seeded target, same kernels):
+# cached so the fp32 and fp64 cases of one shape share one CPU run
+_ORACLE = {}
+
+
+def _oracle_forward(f, d, shape):
+    key = ("fwd", shape)
+    if key not in _ORACLE:
+        t = strip_layout(shape, sum(shape))
+        m = t.astype(np.float64)
+        hf_f, hf_d = o.spectra(f[0], shape), o.spectra(d[0], shape)
+        ints = [o.intensity(m, arrs[0], arrs[1], dose, hf)
+                for arrs, dose, hf in ((f, 1.0, hf_f), (f, 1.02, hf_f), (d, 0.98, hf_d))]
+        pr = o.corners(m, f, d, binarize=False, hf_focus=hf_f, hf_defocus=hf_d)
+        gi = o.ilt_grad(m, pr["nominal"], t, f, hf=hf_f)
+        gp = o.pvb_grad(m, pr["inner"], pr["outer"], t, f, d, hf_focus=hf_f, hf_defocus=hf_d)
+        _ORACLE[key] = (t, m, ints, pr, gi, gp)
+    return _ORACLE[key]
+
+
+def _oracle_history(f, d, shape):
+    key = ("hist", shape)
+    if key not in _ORACLE:
+        t = strip_layout(shape, 7 + sum(shape))
+        _ORACLE[key] = (t, np.array(o.optimize(t, f, d, o.Cfg(max_iters=6, stop_patience=10**9)).history))
+    return _ORACLE[key]
+
+
 def relmax(a, b):
     return np.abs(np.asarray(a) - np.asarray(b)).max() / np.abs(b).max()
 
@@ -76,34 +104,28 @@ def test_tall_forward_and_gradients_vs_oracle(model, prec, shape):
     f, d, F, D = model
     nv.set_precision(prec)
     tol = TOL[prec]
-    t = strip_layout(shape, sum(shape))
-    m = t.astype(np.float64)
-    hf_f, hf_d = o.spectra(f[0], shape), o.spectra(d[0], shape)
-    for arrs, ks, cond, hf in ((f, F, b2.NOMINAL, hf_f), (f, F, b2.OUTER, hf_f), (d, D, b2.INNER, hf_d)):
+    t, m, ints, pr, gi_ref, gp_ref = _oracle_forward(f, d, shape)
+    for ks, cond, ref in ((F, b2.NOMINAL, ints[0]), (F, b2.OUTER, ints[1]), (D, b2.INNER, ints[2])):
         out = b2.aerial_intensity(m, ks, cond)
-        ref = o.intensity(m, arrs[0], arrs[1], cond.dose, hf)
         assert relmax(out, ref) <= tol["i"], (shape, cond.label)
     cfg = b2.OptConfig()
     p = b2.print_corners(m, F, D, cfg, binarize=False)
-    pr = o.corners(m, f, d, binarize=False, hf_focus=hf_f, hf_defocus=hf_d)
     for c in ("nominal", "inner", "outer"):
         assert np.abs(getattr(p, c) - pr[c]).max() <= tol["p"], (shape, c)
     gi = b2.ilt_gradient(m, pr["nominal"], t, F, cfg)
     gp = b2.pvb_gradient(m, pr["inner"], pr["outer"], t, F, D, cfg)
-    assert relmax(gi, o.ilt_grad(m, pr["nominal"], t, f, hf=hf_f)) <= tol["g"], shape
-    assert relmax(gp, o.pvb_grad(m, pr["inner"], pr["outer"], t, f, d, hf_focus=hf_f, hf_defocus=hf_d)) <= tol["g"], shape
+    assert relmax(gi, gi_ref) <= tol["g"], shape
+    assert relmax(gp, gp_ref) <= tol["g"], shape
 
 
 @pytest.mark.parametrize("prec,shape", CASES)
 def test_tall_optimize_history_vs_oracle(model, prec, shape):
     f, d, F, D = model
     tol = TOL[prec]
-    t = strip_layout(shape, 7 + sum(shape))
+    t, hr = _oracle_history(f, d, shape)
     r = b2.optimize(t, F, D, b2.OptConfig(max_iters=6, stop_patience=10**9, precision=prec))
-    ref = o.optimize(t, f, d, o.Cfg(max_iters=6, stop_patience=10**9))
     h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag]
                   for x in r.loss_history])
-    hr = np.array(ref.history)
     assert h.shape == hr.shape == (6, 7)
     assert np.allclose(h[:, :3], hr[:, :3], rtol=tol["h"]), (shape, h[:, :3], hr[:, :3])
     # dt / max|v| are maxima over the whole grid (curvature-dominated pixels)
