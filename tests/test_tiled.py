@@ -282,6 +282,23 @@ def test_several_strips_in_one_process_match_single_tile(axis):
 
 
 @pytest.mark.gpu
+def test_several_strips_with_host_phi0():
+    """phi0 given on the host (windowed per strip) equals the default device
+    TSDF start when phi0 is that TSDF: bit-identical histories and masks."""
+    import paper_2303_12529_b200 as b2
+    from paper_2303_12529_b200 import _native as nv
+    nv.set_precision("fp64")
+    t, f, d = _case()
+    F, D = _ks(f, "focus"), _ks(d, "defocus")
+    cfg = b2.OptConfig(max_iters=5)
+    phi0 = b2.tsdf_from_mask(t, cfg.d_upper, cfg.d_lower)
+    a = tiled.optimize_tiled(t, F, D, cfg, axis=1, strips_per_rank=3)
+    b = tiled.optimize_tiled(t, F, D, cfg, phi0=phi0, axis=1, strips_per_rank=3)
+    assert [h.l_dso for h in a.loss_history] == [h.l_dso for h in b.loss_history]
+    assert np.array_equal(a.final_mask, b.final_mask) and np.array_equal(a.final_phi.phi, b.final_phi.phi)
+
+
+@pytest.mark.gpu
 def test_fp64_column_strips_through_split_plan_match_single_grid():
     """The fp64 configs[4] path in miniature: an 8192 x 1024 tile as three
     8192 x 512 column windows (split plan, complex128) against the same tile
