@@ -145,3 +145,26 @@ def test_split_plan_spectra_vs_oracle(model, prec):
     tol = 1e-12 if prec == "fp64" else 2e-7
     assert np.abs(hf - ref).max() <= tol * np.abs(ref).max(), prec
     assert np.array_equal(sigma, np.asarray(f[1], np.float64))
+
+
+@pytest.mark.parametrize("prec,shape", [("fp64", (8192, 512)), ("fp64", (8192, 1024)), ("fp32", (8192, 2048)),
+                                        ("fp32", (8192, 1024))])
+def test_split_plan_widths_vs_oracle(prec, shape):
+    """Every split-plan item geometry (Q = 4W'/W rows per plane: fp64 W = 512
+    -> Q = 2, W = 1024 -> Q = 1; fp32 W = 1024 -> Q = 2, W = 2048 -> Q = 1)
+    against the oracle, with a small kernel set (4 + 4 kernels, K = 17) to
+    keep the CPU side short: intensity at the three corners and the ILT
+    gradient."""
+    nv.set_precision(prec)
+    tol = TOL[prec]
+    f, d = o.synthetic_kernels(17, 4, 2)
+    F = b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(*f)], "focus")
+    D = b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(*d)], "defocus")
+    t = strip_layout(shape, 3 + sum(shape), n=60)
+    m = t.astype(np.float64)
+    hf_f, hf_d = o.spectra(f[0], shape), o.spectra(d[0], shape)
+    for arrs, ks, cond, hf in ((f, F, b2.NOMINAL, hf_f), (f, F, b2.OUTER, hf_f), (d, D, b2.INNER, hf_d)):
+        assert relmax(b2.aerial_intensity(m, ks, cond), o.intensity(m, arrs[0], arrs[1], cond.dose, hf)) <= tol["i"]
+    z = o.corners(m, f, d, binarize=False, hf_focus=hf_f, hf_defocus=hf_d)["nominal"]
+    gi = b2.ilt_gradient(m, z, t, F, b2.OptConfig())
+    assert relmax(gi, o.ilt_grad(m, z, t, f, hf=hf_f)) <= tol["g"], shape
