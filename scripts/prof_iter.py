@@ -18,13 +18,17 @@ PASSES = [("mask_fft", ("TMaskRowsOp", "TColsOp", "MaskRowsOp", "ColsOp")), ("F1
           ("A2", ("TA2Op", "A2Op")), ("A3", ("A3Op",)), ("levelset", ("k_ls_velocity", "k_ls_update"))]
 
 
-def run(prec, W=3, K=2):
+def run(prec, W=3, K=2, shape=None):
     import numpy as np
     import torch
     import paper_2303_12529_b200 as b2
     from paper_2303_12529_b200 import _native as nv, inputs
     nv.set_precision(prec)
-    clip = inputs.iccad_like_clip(seed=0)
+    if shape is None:
+        clip = inputs.iccad_like_clip(seed=0)
+    else:  # another geometry (e.g. a split plan): a crop of the configs[4] mosaic
+        H, Wd = shape
+        clip = np.ascontiguousarray(inputs.mosaic_tile(range(16), grid=(4, 4))[:H, 2048:2048 + Wd])
     focus, defocus = b2.gen_synthetic_kernels(35, 24, seed=4)
     fk, dk = focus.device(clip.shape, prec), defocus.device(clip.shape, prec)
     c = b2.optimizer._native_cfg(b2.OptConfig(max_iters=W + K + 2, stop_patience=10**9, precision=prec))
@@ -39,7 +43,7 @@ def run(prec, W=3, K=2):
     L.lsopc_session_destroy(s)
 
 
-def summarise(path, prec, per_iter=11):
+def summarise(path, prec, per_iter=11, tag=None):
     rows = list(csv.reader(open(path)))
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hd = rows[h]
@@ -68,13 +72,13 @@ def summarise(path, prec, per_iter=11):
     out["iteration"] = total
     out.update(per_pass)
     out["pass_names"] = {str(i): n for i, (n, _) in enumerate(PASSES)}
-    dst = ROOT / "profiles" / f"traffic_{prec}.json"
+    dst = ROOT / "profiles" / f"traffic_{tag or prec}.json"
     dst.write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":
-    if sys.argv[1] == "--summarise":
-        summarise(sys.argv[2], sys.argv[3])
-    else:
-        run(sys.argv[1])
+    if sys.argv[1] == "--summarise":  # --summarise <csv> <prec> [tag]
+        summarise(sys.argv[2], sys.argv[3], tag=sys.argv[4] if len(sys.argv) > 4 else None)
+    else:  # <prec> [H W]
+        run(sys.argv[1], shape=(int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else None)
