@@ -200,7 +200,7 @@ def _ks(arrs, cond):
     return b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(*arrs)], cond)
 
 
-def _tiled_worker(rank, world, port, q, max_iters, axis=0):
+def _tiled_worker(rank, world, port, q, max_iters, axis=0, spr=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
@@ -211,7 +211,8 @@ def _tiled_worker(rank, world, port, q, max_iters, axis=0):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         t, f, d = _case()
-        r = tiled.optimize_tiled(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=max_iters), axis=axis)
+        r = tiled.optimize_tiled(t, _ks(f, "focus"), _ks(d, "defocus"), b2.OptConfig(max_iters=max_iters), axis=axis,
+                                 strips_per_rank=spr)
         h = np.array([[x.l_ilt, x.l_pvb, x.l_dso, x.dt, x.max_v, x.max_step, x.max_grad_mag] for x in r.loss_history])
         q.put((rank, h, r.final_mask, r.metrics.l2, r.metrics.pvband))
     finally:
@@ -240,6 +241,17 @@ def test_single_strip_is_bit_identical_to_optimize(axis):
     hr, mr, l2, pvb = _reference(12)
     assert np.array_equal(h, hr)
     assert np.array_equal(r.final_mask, mr) and (r.metrics.l2, r.metrics.pvband) == (l2, pvb)
+
+
+@pytest.mark.gpu
+def test_two_ranks_two_strips_each_match_single_tile():
+    """2 ranks x 2 strips (local copies inside a rank, P2P between ranks) on
+    column strips of the 256 x 1024 case."""
+    hr, mr, l2, pvb = _reference(12)
+    for rank, h, mask, l2r, pvbr in _run(2, _tiled_worker, 12, 1, 2, timeout=600):
+        assert np.allclose(h, hr, rtol=1e-9, atol=1e-12)
+        assert np.array_equal(mask, mr)
+        assert (l2r, pvbr) == (l2, pvb)
 
 
 @pytest.mark.gpu
