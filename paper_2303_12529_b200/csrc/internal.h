@@ -21,6 +21,8 @@ struct Grid {
   // virtual 2048 x 4W grid those planes form in memory, and the radix-4
   // combine across the planes folded into the row passes (spectral.cuh).
   int vsplit = 0;
+  // F1 as a tap contraction on the tensor cores (f1_tc.cu; fp32 tier)
+  int tcf1 = 0;
   size_t n() const { return (size_t)H * W; }
   size_t csize() const { return prec == F64 ? 16 : 8; }
   size_t rsize() const { return prec == F64 ? 8 : 4; }
@@ -52,6 +54,10 @@ struct SpecSet {
   void* Ipart;       // 8 groups x 2 sets x H*W elements R
   void* Vpart;       // 8 groups x 2 sets x H*W complex
   unsigned* tick;    // 2 passes x 2 sets x max(H, W) tickets, zero between launches
+  // tensor-core F1 (f1_tc.cu): the taps' row DFT G_k(i, v) / W, [W][K][nk]
+  // complex64 (null: this set runs the FFT F1), and the kernel side K
+  const void* G;
+  int K;
 };
 
 // K0: spectra of nk K x K kernels (float64 transform, stored in plan precision)
@@ -63,16 +69,27 @@ void launch_spec_to_c128(const Grid& g, const void* field, double* out, cudaStre
 
 // M^ = FFT2(mask); exactly one of mask_u8 / mask_f64 / phi (mask = phi <= 0) is non-null.
 // scratch >= H*W complex elements.
+// cols = false: the row pass only (M~ in scratch, for the tensor-core F1)
 void launch_mask_fft(const Grid& g, const uint8_t* mask_u8, const double* mask_f64, const double* phi,
-                     void* mhat, void* scratch, StopFlag stop, cudaStream_t s);
+                     void* mhat, void* scratch, StopFlag stop, cudaStream_t s, bool cols = true);
 
 // forward of nsets (1 or 2) sets: T_k = IFFT_y(M^ H_k)/(HW), I = sum_k w_k |IFFT_x T_k|^2.
 // a0_c128 (nullable): the first set's first field A_0 as complex128 row-major.
 void launch_forward(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, double* a0_c128,
                     StopFlag stop, cudaStream_t s);
 
-// the two halves of launch_forward / launch_adjoint (per-pass timing)
-void launch_f1(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
+// the two halves of launch_forward / launch_adjoint (per-pass timing).
+// launch_f1 runs the tensor-core F1 on mtilde (the mask's row transform, the
+// mask pass's scratch) when use_tc_f1(), else the FFT F1 on mhat.
+void launch_f1(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s,
+               const void* mtilde = nullptr);
+
+// tensor-core F1 (f1_tc.cu)
+bool tcf1_plan_ok(int H, int W, int prec, int vsplit);
+bool tcf1_kset_ok(int nk, int K);
+bool use_tc_f1(const Grid& g, const SpecSet* sets, int nsets);
+void launch_tap_rows(const Grid& g, int nk, int K, const double* coeffs_dev, void* G, cudaStream_t s);
+void launch_f1_tc(const Grid& g, const void* mtilde, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
 void launch_f2(const Grid& g, const SpecSet* sets, int nsets, double* a0_c128, StopFlag stop, cudaStream_t s);
 void launch_a1(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);
 void launch_a2(const Grid& g, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s);

@@ -107,8 +107,12 @@ struct lsopc_kset {
   lsopc_plan* plan = nullptr;
   int nk = 0, K = 0;
   DevBuf spec;
+  DevBuf G;  // tensor-core F1: the taps' row DFT (f1_tc.cu), when the plan and the set allow it
   std::vector<double> w;
-  ~lsopc_kset() { spec.release(); }
+  ~lsopc_kset() {
+    spec.release();
+    G.release();
+  }
 };
 
 namespace {
@@ -155,15 +159,28 @@ SpecSet spec_set(lsopc_plan* p, const lsopc_kset* ks, int which, size_t T_off_ke
   s.Ipart = p->Ipart.p;
   s.Vpart = p->Vpart.p;
   s.tick = p->tick.as<unsigned>();
+  s.G = ks->G.p;
+  s.K = ks->K;
   return s;
 }
 
-// forward of one set (I into If) or of focus + defocus (If, Id)
+// the mask's transform and F1 of nsets sets: the tensor-core F1 reads the
+// mask pass's row transform (scratch), the FFT F1 its full 2-D transform
+void mask_and_f1(lsopc_plan* p, const SpecSet* sets, int nsets, const uint8_t* mu8, const double* mf,
+                 const double* phi, StopFlag stop, cudaStream_t s) {
+  const bool tc = use_tc_f1(p->g, sets, nsets);
+  launch_mask_fft(p->g, mu8, mf, phi, p->mhat.p, p->scratch.p, stop, s, !tc);
+  launch_f1(p->g, p->mhat.p, sets, nsets, stop, s, p->scratch.p);
+}
+
+// forward of one set (I into If) or of focus + defocus (If, Id) from a mask
+// (exactly one of mu8 / mf / phi non-null)
 void forward(lsopc_plan* p, const lsopc_kset* f, const lsopc_kset* d, StopFlag stop, cudaStream_t s,
-             double* a0_c128 = nullptr) {
+             const uint8_t* mu8, const double* mf, const double* phi, double* a0_c128 = nullptr) {
   p->ensure_T(f->nk + (d ? d->nk : 0));
   SpecSet sets[2] = {spec_set(p, f, 0, 0), d ? spec_set(p, d, 1, f->nk) : SpecSet{}};
-  launch_forward(p->g, p->mhat.p, sets, d ? 2 : 1, a0_c128, stop, s);
+  mask_and_f1(p, sets, d ? 2 : 1, mu8, mf, phi, stop, s);
+  launch_f2(p->g, sets, d ? 2 : 1, a0_c128, stop, s);
   ck_launch("forward");
 }
 
@@ -203,6 +220,7 @@ int lsopc_plan_create(int H, int W, int precision, lsopc_plan** out) {
       p->g.lgW = ilog2(W);
       p->g.prec = precision;
       p->g.vsplit = vsplit ? 1 : 0;
+      p->g.tcf1 = tcf1_plan_ok(H, W, p->g.prec, p->g.vsplit) ? 1 : 0;
       const int nmax = H > W ? H : W;
       p->g.lgnmax = ilog2(nmax);
       std::vector<double> t64(2 * nmax);
@@ -282,6 +300,11 @@ int lsopc_kset_create(lsopc_plan* plan, int n_k, int K, const double* coeffs_hos
       ck(cudaMemcpyAsync(coeffs.p, coeffs_host, cb, cudaMemcpyHostToDevice, s), "memcpy");
       launch_kernel_spectra(plan->g, n_k, K, coeffs.as<double>(), ks->spec.p, plan->scratch.p, plan->scratch2.p, s);
       ck_launch("kernel spectra");
+      if (plan->g.tcf1 && tcf1_kset_ok(n_k, K)) {
+        ks->G.ensure((size_t)plan->g.W * K * n_k * 8);
+        launch_tap_rows(plan->g, n_k, K, coeffs.as<double>(), ks->G.p, s);
+        ck_launch("tap rows");
+      }
       ck(cudaStreamSynchronize(s), "sync");
       coeffs.release();
     } catch (...) {
@@ -319,9 +342,7 @@ int lsopc_aerial_intensity(lsopc_plan* plan, const lsopc_kset* ks, const double*
     check_plan(plan);
     check_kset(plan, ks);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_mask_fft(plan->g, nullptr, mask_dev, nullptr, plan->mhat.p, plan->scratch.p, nullptr, s);
-    ck_launch("mask fft");
-    forward(plan, ks, nullptr, nullptr, s);
+    forward(plan, ks, nullptr, nullptr, s, nullptr, mask_dev, nullptr);
     launch_scale_intensity(plan->g, plan->If.p, dose, out_dev, s);
     ck_launch("scale intensity");
   });
@@ -335,9 +356,7 @@ int lsopc_print_corners(lsopc_plan* plan, const lsopc_kset* focus, const lsopc_k
     check_kset(plan, focus);
     check_kset(plan, defocus);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_mask_fft(plan->g, nullptr, mask_dev, nullptr, plan->mhat.p, plan->scratch.p, nullptr, s);
-    ck_launch("mask fft");
-    forward(plan, focus, defocus, nullptr, s);
+    forward(plan, focus, defocus, nullptr, s, nullptr, mask_dev, nullptr);
     ResistParams rp{i_th, sigma_z, 0.0, 0.0};
     if (binarize)
       launch_resist(plan->g, plan->If.p, plan->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr,
@@ -358,9 +377,7 @@ int lsopc_socs_gradient(lsopc_plan* plan, const lsopc_kset* ks, const double* ma
     check_kset(plan, ks);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t n = plan->n();
-    launch_mask_fft(plan->g, nullptr, mask_dev, nullptr, plan->mhat.p, plan->scratch.p, nullptr, s);
-    ck_launch("mask fft");
-    forward(plan, ks, nullptr, nullptr, s);
+    forward(plan, ks, nullptr, nullptr, s, nullptr, mask_dev, nullptr);
     launch_gate(plan->g, z_dev, zt_dev, 1.0, plan->wf.p, s);
     ck_launch("gate");
     SpecSet set = spec_set(plan, ks, 0, 0);
@@ -378,9 +395,7 @@ int lsopc_convolve(lsopc_plan* plan, const lsopc_kset* ks, const double* mask_de
     check_plan(plan);
     check_kset(plan, ks);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_mask_fft(plan->g, nullptr, mask_dev, nullptr, plan->mhat.p, plan->scratch.p, nullptr, s);
-    ck_launch("mask fft");
-    forward(plan, ks, nullptr, nullptr, s, out_c128_dev);
+    forward(plan, ks, nullptr, nullptr, s, nullptr, mask_dev, nullptr, out_c128_dev);
   });
 }
 
@@ -559,9 +574,10 @@ void enqueue_iteration(lsopc_session* ss, int par, cudaStream_t s, cudaEvent_t* 
 
   // forward: M^ -> T_k -> I_f, I_d -> resist, losses, gates
   mark(0);
-  launch_mask_fft(g, ss->mask.as<uint8_t>(), nullptr, nullptr, p->mhat.p, p->scratch.p, stop, s);
+  const bool tc = use_tc_f1(g, sets, 2);
+  launch_mask_fft(g, ss->mask.as<uint8_t>(), nullptr, nullptr, p->mhat.p, p->scratch.p, stop, s, !tc);
   mark(1);
-  launch_f1(g, p->mhat.p, sets, 2, stop, s);
+  launch_f1(g, p->mhat.p, sets, 2, stop, s, p->scratch.p);
   mark(2);
   launch_f2(g, sets, 2, nullptr, stop, s);
   mark(3);
@@ -622,8 +638,7 @@ void enqueue_phase(lsopc_session* ss, int phase, cudaStream_t s) {
   SpecSet sets[2] = {spec_set(p, ss->focus, 0, 0), spec_set(p, ss->defocus, 1, ss->focus->nk)};
   switch (phase) {
     case 0: {  // forward from phi (the halo columns were refreshed by the caller) -> sum losses
-      launch_mask_fft(g, nullptr, nullptr, ss->phi.as<double>(), p->mhat.p, p->scratch.p, stop, s);
-      launch_f1(g, p->mhat.p, sets, 2, stop, s);
+      mask_and_f1(p, sets, 2, nullptr, nullptr, ss->phi.as<double>(), stop, s);
       launch_f2(g, sets, 2, nullptr, stop, s);
       ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
       launch_resist(g, p->If.p, p->Id.p, ss->target.as<uint8_t>(), nullptr, rp, p->wf.p, p->wd.p, nullptr,
@@ -840,8 +855,7 @@ int lsopc_session_finish(lsopc_session* ss, double* best_phi_dev, uint8_t* final
       l2 = h.best_l2;
       pvb = h.best_pvb;
     } else {
-      launch_mask_fft(g, fm, nullptr, nullptr, p->mhat.p, p->scratch.p, nullptr, s);
-      forward(p, ss->focus, ss->defocus, nullptr, s);
+      forward(p, ss->focus, ss->defocus, nullptr, s, fm, nullptr, nullptr);
       uint8_t* hn = p->hard.as<uint8_t>();
       ResistParams rp{ss->cfg.i_th, ss->cfg.sigma_z, 0.0, 0.0};
       launch_resist(g, p->If.p, p->Id.p, nullptr, nullptr, rp, nullptr, nullptr, nullptr, nullptr, nullptr, hn,
@@ -878,8 +892,7 @@ int lsopc_session_losses(lsopc_session* ss, double* l_ilt, double* l_pvb, double
     cudaStream_t s = ss->s;
     SpecSet sets[2] = {spec_set(p, ss->focus, 0, 0), spec_set(p, ss->defocus, 1, ss->focus->nk)};
     // _forward_losses on mask_from_phi(phi) (optimizer.py:172-177, 334-336); not gated by the stop flag
-    launch_mask_fft(g, nullptr, nullptr, ss->phi.as<double>(), p->mhat.p, p->scratch.p, nullptr, s);
-    launch_f1(g, p->mhat.p, sets, 2, nullptr, s);
+    mask_and_f1(p, sets, 2, nullptr, nullptr, ss->phi.as<double>(), nullptr, s);
     launch_f2(g, sets, 2, nullptr, nullptr, s);
     ResistParams rp{c.i_th, c.sigma_z, c.alpha, c.beta};
     ss->scalars.ensure(8 * sizeof(double));

@@ -79,14 +79,20 @@ __global__ void k_dft_cols_split(int K, int H, int W, int lgT, int lgnmax, const
 int finish_max_blocks() { return 148 * 2; }
 
 void launch_mask_fft(const Grid& g, const uint8_t* mu8, const double* mf, const double* phi, void* mhat,
-                     void* scratch, StopFlag stop, cudaStream_t s) {
+                     void* scratch, StopFlag stop, cudaStream_t s, bool cols) {
   const void* src = mu8 ? (const void*)mu8 : mf ? (const void*)mf : (const void*)phi;
   const int kind = mu8 ? SRC_U8 : mf ? SRC_F64 : SRC_PHI;
-  if (g.prec == F64) mask_fft_impl<double>(g, src, kind, mhat, scratch, stop, s);
-  else mask_fft_impl<float>(g, src, kind, mhat, scratch, stop, s);
+  void* out = cols ? mhat : nullptr;  // null: the row pass only
+  if (g.prec == F64) mask_fft_impl<double>(g, src, kind, out, scratch, stop, s);
+  else mask_fft_impl<float>(g, src, kind, out, scratch, stop, s);
 }
 
-void launch_f1(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s) {
+void launch_f1(const Grid& g, const void* mhat, const SpecSet* sets, int nsets, StopFlag stop, cudaStream_t s,
+               const void* mtilde) {
+  if (mtilde && use_tc_f1(g, sets, nsets)) {
+    launch_f1_tc(g, mtilde, sets, nsets, stop, s);
+    return;
+  }
   if (g.prec == F64) f1_impl<double>(g, mhat, sets, nsets, stop, s);
   else f1_impl<float>(g, mhat, sets, nsets, stop, s);
 }

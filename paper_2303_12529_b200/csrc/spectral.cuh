@@ -2036,6 +2036,7 @@ void mask_fft_impl(const Grid& g, const void* src, int kind, void* mhat, void* s
     mr.nitems = g.H >> sh.lgR;
     launch_op<R>(mr, row_threads(sh), 0, stop, s);
   }
+  if (!mhat) return;  // the row pass only (M~ for the tensor-core F1)
   if (g.vsplit) {  // columns of the virtual 2048 x 4W grid
     const Grid gv = vs_grid(g);
     sh = shape_of<R>(gv);
