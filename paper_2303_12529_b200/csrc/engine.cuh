@@ -35,12 +35,15 @@ namespace eng {
 // 16 complex values per thread in both precisions (radix-16 stages); a CTA
 // is 512 threads for complex64 (<= 128 registers) and 256 threads for
 // complex128 (<= 255 registers), i.e. 64 KB of operands per stage buffer.
-template <typename C> constexpr int P_of() { return 16; }
-template <typename C> constexpr int LGP_of() { return 4; }
+#ifndef LSB_C128_LGP  // experiment builds may give complex128 8 values per thread (-DLSB_C128_LGP=3: 512 threads)
+#define LSB_C128_LGP 4
+#endif
+template <typename C> constexpr int LGP_of() { return sizeof(C) == 8 ? 4 : LSB_C128_LGP; }
+template <typename C> constexpr int P_of() { return 1 << LGP_of<C>(); }
 #ifndef LSB_C64_THREADS  // experiment builds may shrink the complex64 CTA (LSB_DEFINES=-DLSB_C64_THREADS=256)
 #define LSB_C64_THREADS 512
 #endif
-template <typename C> constexpr int cta_threads() { return sizeof(C) == 8 ? LSB_C64_THREADS : 256; }
+template <typename C> constexpr int cta_threads() { return sizeof(C) == 8 ? LSB_C64_THREADS : 4096 / P_of<C>(); }
 
 // ---- radix-R DFTs in registers, forward sign (exp(-2 pi i rk/R)), natural order out
 
