@@ -233,11 +233,11 @@ def exchange_local_halos(phis, strips, wrap):
         P = _lines(phis[j], s)
         if j > 0 or wrap:
             L = strips[j - 1]
-            l0, l1 = L.interior
+            _, l1 = L.interior
             P[:, i0 - h:i0].copy_(_lines(phis[j - 1], L)[:, l1 - h:l1])
         if j < k - 1 or wrap:
             R = strips[(j + 1) % k]
-            r0, r1 = R.interior
+            r0, _ = R.interior
             P[:, i1:i1 + h].copy_(_lines(phis[(j + 1) % k], R)[:, r0:r0 + h])
 
 
