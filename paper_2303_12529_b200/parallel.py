@@ -116,12 +116,25 @@ def optimize_batch(targets, focus_kernels, defocus_kernels, cfg, group=None, sol
             nv.set_lane(lane)
             torch.cuda.set_device(dev)
             stream = torch.cuda.Stream()
+            # the shot count runs on a host tail thread; a clip is assembled
+            # (waiting for its count) only after the lane's next clip has run,
+            # so the count never stalls the lane
+            pending = None
+
+            def flush(p):
+                r = _assemble(p[1], cfg)
+                with lock:
+                    record(p[0], r)
+
             with torch.cuda.stream(stream):
                 for i, target in items:
-                    r = _assemble(_optimize_device(target, focus_kernels, defocus_kernels, cfg, shots_on="host"), cfg)
-                    with lock:
-                        record(i, r)
+                    parts = _optimize_device(target, focus_kernels, defocus_kernels, cfg, shots_on="host")
+                    if pending is not None:
+                        flush(pending)
+                    pending = (i, parts)
             stream.synchronize()
+            if pending is not None:
+                flush(pending)
 
         with ThreadPoolExecutor(max_workers=lanes) as pool:
             for f in [pool.submit(worker, l, mine[l::lanes]) for l in range(lanes)]:
