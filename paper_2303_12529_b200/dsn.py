@@ -117,14 +117,22 @@ def refine_batch(targets, phi0, m, focus_kernels, defocus_kernels, cfg, lanes=2)
     torch = _torch()
     results = [None] * len(targets)
 
-    def solve(i):
-        return _assemble(_optimize_device(targets[i], focus_kernels, defocus_kernels, cfg, phi0=phi0[i],
-                                          modulation=m[i], shots_on="host"), cfg)
+    def run_lane(idx):
+        # each clip is assembled (waiting for its host shot count) after the
+        # lane's next clip has run, so the count never stalls the lane
+        pending = None
+        for i in idx:
+            parts = _optimize_device(targets[i], focus_kernels, defocus_kernels, cfg, phi0=phi0[i], modulation=m[i],
+                                     shots_on="host")
+            if pending is not None:
+                results[pending[0]] = _assemble(pending[1], cfg)
+            pending = (i, parts)
+        if pending is not None:
+            results[pending[0]] = _assemble(pending[1], cfg)
 
     lanes = max(1, min(int(lanes), len(targets)))
     if lanes == 1:
-        for i in range(len(targets)):
-            results[i] = solve(i)
+        run_lane(range(len(targets)))
         return results
     from concurrent.futures import ThreadPoolExecutor
     from . import _native as nv
@@ -137,8 +145,7 @@ def refine_batch(targets, phi0, m, focus_kernels, defocus_kernels, cfg, lanes=2)
         stream = torch.cuda.Stream()
         stream.wait_stream(producer)  # phi0 / m were written on the caller's stream
         with torch.cuda.stream(stream):
-            for i in range(lane, len(targets), lanes):
-                results[i] = solve(i)
+            run_lane(range(lane, len(targets), lanes))
         stream.synchronize()
 
     with ThreadPoolExecutor(max_workers=lanes) as pool:
