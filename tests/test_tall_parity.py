@@ -168,3 +168,17 @@ def test_split_plan_widths_vs_oracle(prec, shape):
     z = o.corners(m, f, d, binarize=False, hf_focus=hf_f, hf_defocus=hf_d)["nominal"]
     gi = b2.ilt_gradient(m, z, t, F, b2.OptConfig())
     assert relmax(gi, o.ilt_grad(m, z, t, f, hf=hf_f)) <= tol["g"], shape
+
+
+def test_fp64_plan_limits():
+    """The fp64 tier takes 8192 x W grids for 256 <= W <= 1024 (split plan)
+    and rejects wider 8192-row grids and 8192-point rows with ValueError
+    (the plan's message names the limit)."""
+    nv.set_precision("fp64")
+    f, d = o.synthetic_kernels(7, 1, 0)
+    F = b2.KernelSet([b2.OpticalKernel(c, float(w)) for c, w in zip(*f)], "focus")
+    for shape in ((8192, 2048), (256, 8192)):
+        with pytest.raises(ValueError, match="FP64 tier"):
+            b2.aerial_intensity(np.zeros(shape), F)
+    out = b2.aerial_intensity(np.zeros((8192, 512)), F)
+    assert out.shape == (8192, 512) and not out.any()
