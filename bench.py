@@ -370,9 +370,25 @@ def b200_arm(args, world, rank, local):
     t_e2e = parallel.max_over_ranks(time_e2e(b2, clip, focus, defocus, K, args.precision), device="cuda")
     e2e_val = world * K / t_e2e
 
+    def guard(fn):
+        """A failed sub-line is reported in place and must not cost the
+        headline line (one process; with several ranks an exception still
+        propagates, since the other ranks' collectives would wait for it)."""
+        if world > 1:
+            return fn()
+        try:
+            return fn()
+        except Exception as e:
+            import traceback
+            traceback.print_exc()
+            try:
+                torch.cuda.synchronize()
+            except Exception:
+                pass
+            return {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+
     # ---- config 2: full default solve of this rank's clip (latency) ----------
-    solve = batch = None
-    if not args.no_solve:
+    def sec_solve():
         # warm-up solve on another clip: the first call with a new OptConfig
         # allocates the session buffers and captures the iteration graphs
         lat, rs = time_solve(b2, clip, inputs.iccad_like_clip(seed=1000 + rank), focus, defocus, args.precision)
@@ -403,25 +419,33 @@ def b200_arm(args, world, rank, local):
         solve["extensions"] = {"note": "opt-in OptConfig(grad_scheme='upwind') / reinit_every=5 (phi <- exact TSDF "
                                        "of its mask); not in the reference, parity against the oracle's "
                                        "restatement only", **ext}
-        # ---- config 3: a batch of clips sharded clip-parallel, no collective ---
+        return solve
+
+    # ---- config 3: a batch of clips sharded clip-parallel, no collective -----
+    def sec_batch():
+        # warm-up: every lane builds its spectra and session once
+        parallel.warm_lanes(inputs.iccad_like_clip(seed=2000 + rank), focus, defocus,
+                            b2.OptConfig(precision=args.precision))
+        clips = parallel.LazyClips(args.clips, seed0=0)
+        recs, secs = parallel.optimize_batch(clips, focus, defocus, b2.OptConfig(precision=args.precision),
+                                             synchronize=torch.cuda.synchronize)
+        batch = {"clips": args.clips, "seconds": round(secs, 3), "clips_per_s": round(args.clips / secs, 3),
+                 "iters_total": int(sum(x.iters for x in recs)),
+                 "iters_per_s": round(sum(x.iters for x in recs) / secs, 2),
+                 "mean_l2": round(float(np.mean([x.l2 for x in recs])), 1),
+                 "mean_pvband": round(float(np.mean([x.pvband for x in recs])), 1),
+                 "note": f"iccad_like_clip(0..{args.clips - 1}) round-robin over {world} GPU(s), "
+                         "2 concurrent streams per GPU, default OptConfig, each clip solved to the stop rule"}
+        return batch
+
+    solve = batch = None
+    if not args.no_solve:
+        solve = guard(sec_solve)
         if args.clips > 0:
-            # warm-up: every lane builds its spectra and session once
-            parallel.warm_lanes(inputs.iccad_like_clip(seed=2000 + rank), focus, defocus,
-                                b2.OptConfig(precision=args.precision))
-            clips = parallel.LazyClips(args.clips, seed0=0)
-            recs, secs = parallel.optimize_batch(clips, focus, defocus, b2.OptConfig(precision=args.precision),
-                                                 synchronize=torch.cuda.synchronize)
-            batch = {"clips": args.clips, "seconds": round(secs, 3), "clips_per_s": round(args.clips / secs, 3),
-                     "iters_total": int(sum(x.iters for x in recs)),
-                     "iters_per_s": round(sum(x.iters for x in recs) / secs, 2),
-                     "mean_l2": round(float(np.mean([x.l2 for x in recs])), 1),
-                     "mean_pvband": round(float(np.mean([x.pvband for x in recs])), 1),
-                     "note": f"iccad_like_clip(0..{args.clips - 1}) round-robin over {world} GPU(s), "
-                             "2 concurrent streams per GPU, default OptConfig, each clip solved to the stop rule"}
+            batch = guard(sec_batch)
 
     # ---- config 4: DevelSet-Net (random init) + GPU level-set refinement -----
-    instant = None
-    if args.dsn_batch > 0 and not args.no_solve:
+    def sec_instant():
         from paper_2303_12529_b200 import dsn
         net = dsn.build_net()
         cfg_d = b2.OptConfig(precision=args.precision)
@@ -437,10 +461,14 @@ def b200_arm(args, world, rank, local):
                    "mean_l2": round(float(np.mean([x.metrics.l2 for x in ri.results])), 1),
                    "note": "random-init two-branch UNet (bf16) -> fused clip + AHF -> DSO per clip to the stop "
                            "rule (configs[3]); per rank"}
+        return instant
+
+    instant = None
+    if args.dsn_batch > 0 and not args.no_solve:
+        instant = guard(sec_instant)
 
     # ---- modulation_search, candidates sharded ---------
-    modsearch = None
-    if args.modsearch > 0 and not args.no_solve:
+    def sec_modsearch():
         cfg_m = b2.OptConfig(precision=args.precision)
         tgt = inputs.iccad_like_clip(seed=0)
         phi_gt = b2.tsdf_from_mask(tgt)
@@ -455,10 +483,14 @@ def b200_arm(args, world, rank, local):
                      "note": f"modulation_search(TSDF of iccad_like_clip(0), 41 shifts of the gate, 10 "
                              f"curvature-on iterations each, device-side final L_DSO); candidates round-robin "
                              f"over {world} GPU(s), 2 streams per GPU, one all-gather of the scores"}
+        return modsearch
+
+    modsearch = None
+    if args.modsearch > 0 and not args.no_solve:
+        modsearch = guard(sec_modsearch)
 
     # ---- config 5: one oversized tile split into strips over the ranks -------
-    tile = None
-    if args.tile > 0 and not args.no_solve:
+    def sec_tile():
         from paper_2303_12529_b200 import tiled
         T = args.tile
         g = T // N_SIDE
@@ -483,12 +515,18 @@ def b200_arm(args, world, rank, local):
 
         tile = run_tile(args.precision)
         if not args.no_tier:
-            tile["tiers"] = {p: run_tile(p) for p in ("fp32", "fp64") if p != args.precision}
+            tile["tiers"] = {p: guard(lambda p=p: run_tile(p)) for p in ("fp32", "fp64") if p != args.precision}
+        return tile
+
+    tile = None
+    if args.tile > 0 and not args.no_solve:
+        tile = guard(sec_tile)
 
     # ---- the reference's own precision (fp64 tier: complex128 transforms) -----
-    tiers = {}
     other = "fp64" if args.precision == "fp32" else "fp32"
-    if not args.no_tier:
+
+    def sec_tiers():
+        tiers = {}
         ms_o, ms_o_max, sess_o, _ = time_session(b2, nv, L, sp, focus, defocus, clip, K, W, other, world, dist)
         L.lsopc_session_destroy(sess_o)
         b_o = algorithmic_bytes_per_iter(n, 2 * N_K, other)
@@ -508,10 +546,12 @@ def b200_arm(args, world, rank, local):
                 "shots": ro.metrics.shots}
         tiers[other]["note"] = (f"same workload as the headline in the {other} tier; device iters/s over {K} "
                                 f"steps, e2e through b2.optimize, full default solve")
+        return tiers
+
+    tiers = guard(sec_tiers) if not args.no_tier else {}
 
     # ---- configs[0]: 512^2 two bars, 24 + 24 kernels, 50 iterations ---------
-    config0 = None
-    if not args.no_config0:
+    def sec_config0():
         bars = inputs.two_bar_layout()
         c0 = {}
         for prec in (args.precision, other):
@@ -527,6 +567,11 @@ def b200_arm(args, world, rank, local):
                                "OptConfig(max_iters=50, stop_patience=1e9) for iters/s (device: 50 graph-replayed "
                                "iterations; e2e: b2.optimize from the host target), plus the default solve "
                                "(reference: 17 iterations, l2 52, pvband 148, shots 102)", **c0}
+        return config0
+
+    config0 = None
+    if not args.no_config0:
+        config0 = guard(sec_config0)
 
     if rank != 0:
         if world > 1:
