@@ -182,3 +182,17 @@ def test_fp64_plan_limits():
             b2.aerial_intensity(np.zeros(shape), F)
     out = b2.aerial_intensity(np.zeros((8192, 512)), F)
     assert out.shape == (8192, 512) and not out.any()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_split_plan_convolve_vs_numpy(prec):
+    """fields.convolve (fields.py:77-87) on a split plan (8192 x 256): the
+    field A_0 comes out of the split F2 in natural row order."""
+    nv.set_precision(prec)
+    f, _ = o.synthetic_kernels(11, 1, 5)
+    k = f[0][0]
+    t = strip_layout((8192, 256), 99, n=30).astype(np.float64)
+    out = b2.convolve(t, b2.OpticalKernel(k, 1.0))
+    ref = np.fft.ifft2(np.fft.fft2(t) * np.fft.fft2(o.embed(k, t.shape)))
+    tol = 1e-12 if prec == "fp64" else 2e-6
+    assert np.abs(out - ref).max() <= tol * np.abs(ref).max(), prec
